@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: FISTA iterations/s (and edges/s, GB/s vs the HBM roofline) of the
+B200 solver on BASELINE configurations, one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1: NCCL row-sharded solver)
+
+One "step" = one FISTA iteration (BASELINE metric) over the whole graph.
+Workload (default): BASELINE config C -- power-law citation-like graph,
+n = 10M nodes, 200M undirected edge draws, k = 32, FISTA, row-partitioned
+across the N GPUs (strong scaling: the graph is fixed as N grows).
+Inputs (CSR 1.7 GB, U 2.6 GB per replica) are far larger than the 126 MB L2,
+so no explicit flush is needed between timed iterations.
+
+--impl reference times the UNMODIFIED reference CPU solver (oracle/_ref, built
+from /root/reference headers) on the same graph and metric, with all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (kind, n, m, C, method, extra)
+    "A": dict(kind="sbm", n=10_000, m=200_000, c=8, blocks=8, method="gpa"),
+    "B": dict(kind="sbm", n=1_000_000, m=20_000_000, c=16, blocks=16, method="fista_bt"),
+    "C": dict(kind="citation", n=10_000_000, m=200_000_000, c=32, method="fista"),
+    "D": dict(kind="citation", n=70_000_000, m=1_000_000_000, c=32, method="fista"),
+    "E8": dict(kind="citation", n=4_000_000, m=80_000_000, c=8, method="fista"),
+    "E32": dict(kind="citation", n=4_000_000, m=80_000_000, c=32, method="fista"),
+    "E64": dict(kind="citation", n=4_000_000, m=80_000_000, c=64, method="fista"),
+    "E128": dict(kind="citation", n=4_000_000, m=80_000_000, c=128, method="fista"),
+}
+GRAPH_SEED = 1
+X0_SEED = 1
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_graph(cfg, threads=0):
+    import paper_2506_04045_b200 as fc
+    if cfg["kind"] == "sbm":
+        return fc.generate_sbm(cfg["n"], cfg["m"], cfg["blocks"], seed=GRAPH_SEED, p_in=0.9, locality=False,
+                               threads=threads)
+    return fc.generate_citation(cfg["n"], cfg["m"], seed=GRAPH_SEED, alpha=2.5, gamma=2.0, locality=False,
+                                threads=threads)
+
+
+def bytes_model(n, nnz, c, method, weighted=False):
+    """Algorithmic bytes.
+
+    iteration: B = 8(N+1) + 12 nnz + g*8*C*nnz + s*8*C*N  with g=2, s=6 (FISTA) or g=1, s=3 (GPA)
+    sweep kernel (per launch, our layout): row_ptr 8(N+1) + col 4 nnz (+8 nnz values if weighted)
+       + g gathers 8*C*nnz + own row 8*C*N + xs writes g*8*C*N + prod 8 N
+    """
+    g = 1 if method == "gpa" else 2
+    s = 3 if method == "gpa" else 6
+    it = 8 * (n + 1) + 12 * nnz + g * 8 * c * nnz + s * 8 * c * n
+    sweep = 8 * (n + 1) + (12 if weighted else 4) * nnz + g * 8 * c * nnz + 8 * c * n + g * 8 * c * n + 8 * n
+    return it, sweep
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for k, name in enumerate(names):
+                if p[5 + k].lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return world, rank, local
+
+
+def allmax(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_run(cfg, graph, x0, budget_s, iters_wanted):
+    """The reference's own run_fista/run_gpa (oracle/_ref), all host cores, on the
+    same graph; stops after a time-bounded number of iterations."""
+    from oracle import FISTA, GPA, Reference, reference_available
+    if not reference_available():
+        return None
+    ref = Reference()
+    cores = os.cpu_count() or 1
+    workers = ref.lib.fcref_resolve_workers(cores)
+    sim = ref.similarity(graph, fast=True)
+    method = GPA if cfg["method"] == "gpa" else FISTA
+    # probe: one iteration to size the sample
+    t0 = time.perf_counter()
+    r = sim.solve(x0, method=method, max_iter=1, fista_restart=True, workers=workers, want_x=False)
+    probe = time.perf_counter() - t0
+    el = r["elapsed_ms"]
+    per_it = (el[-1] - el[0]) / 1e3 if len(el) >= 2 and el[-1] > el[0] else probe
+    iters = int(max(1, min(iters_wanted, budget_s // max(per_it, 1e-9))))
+    if iters > 1:
+        r = sim.solve(x0, method=method, max_iter=iters, fista_restart=True, workers=workers, want_x=False)
+        el = r["elapsed_ms"]
+    t_it = (el[-1] - el[0]) / 1e3 / max(1, len(el) - 1)
+    return {"s_per_iter": t_it, "iters": len(el) - 1, "cores": int(workers), "probe_s": probe}
+
+
+def run_reference_arm(args, cfg):
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return 0
+    import paper_2506_04045_b200 as fc
+    graph = make_graph(cfg)
+    from oracle import Reference, reference_available
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfcref.so not built"}))
+        return 0
+    ref = Reference()
+    x0 = ref.init_membership(cfg["n"], cfg["c"], 0, X0_SEED, 0)
+    budget = float(os.environ.get("FC_REF_BUDGET_S", "150"))
+    res = cpu_reference_run(cfg, graph, x0, budget, args.steps + args.warmup)
+    value = 1.0 / res["s_per_iter"]
+    it_b, _ = bytes_model(graph.n, graph.nnz, cfg["c"], cfg["method"])
+    sample = (f"full config {args.config} graph (n={graph.n}, nnz={graph.nnz}), {res['iters']} "
+              f"{cfg['method'].upper()} iteration(s) of the reference run_fista/run_gpa, time-bounded to "
+              f"~{budget:.0f}s, {res['cores']} worker threads")
+    line = {
+        "impl": "reference", "metric": "fista_iterations_per_s" if cfg["method"] != "gpa" else "gpa_iterations_per_s",
+        "value": value, "unit": "iter/s", "n_gpus": args.gpus, "steps": res["iters"], "warmup": 0,
+        "ms_per_step": res["s_per_iter"] * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": config_name(args.config, cfg), "n": graph.n, "nnz": graph.nnz, "k": cfg["c"]},
+        "edges_per_s": graph.nnz * value, "achieved_gbs": it_b * value / 1e9,
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": res["cores"], "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def config_name(name, cfg):
+    return (f"config {name}: {cfg['kind']} n={cfg['n']}, {cfg['m']} edge draws, k={cfg['c']}, "
+            f"{cfg['method'].upper()}")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("FC_BENCH_CONFIG", "C"), choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world, rank, local = dist_setup(args)
+    import torch
+    import paper_2506_04045_b200 as fc
+    from paper_2506_04045_b200 import capi
+
+    torch.cuda.set_device(local)
+    t_setup = time.perf_counter()
+    graph = make_graph(cfg)
+    t_graph = time.perf_counter() - t_setup
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [capi.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = capi.Context(local, rank=rank, world=world, nccl_id=nccl_id)
+    x0 = fc.init_membership(cfg["n"], cfg["c"], fc.InitStrategy(fc.InitKind.kRandom, X0_SEED), ctx=ctx)
+    ctx.upload(graph)
+    bounds = ctx.partition()
+    method = {"gpa": capi.GPA, "fista": capi.FISTA, "fista_bt": capi.FISTA_BT}[cfg["method"]]
+    total = args.warmup + args.steps
+    step0 = 0.0
+    if method == capi.FISTA_BT:
+        # start from 20x the Lipschitz-safe step so the line search has work to do
+        step0 = 20.0 * fc.default_step_size(graph, graph.n)
+    scfg = capi.Context.config(method=method, step_size=step0, max_iter=total + 1, fista_restart=True)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
+
+    # ---- device-resident timing --------------------------------------------------------
+    ctx.begin(x0, scfg)
+    ctx.run(args.warmup)
+    ctx.sync()
+    ctx.set_profiling(True)
+    launches0 = ctx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        ctx.run(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = ctx.launch_count() - launches0
+    kt = ctx.kernel_times()
+    ctx.set_profiling(False)
+    ms_local = ev0.elapsed_time(ev1)
+    done = ctx.sync()
+    res = ctx.end(graph.n, cfg["c"], want_x=False)
+    ms = allmax(ms_local, world)
+    iters_done = res["iterations"]
+    valid_count = (iters_done == total) if method != capi.FISTA_BT else True
+    value = args.steps / (ms / 1e3)
+
+    # ---- end to end through the public call (host buffers) -------------------------------
+    e2e = None
+    if not args.no_e2e:
+        ecfg = capi.Context.config(method=method, step_size=step0, max_iter=args.steps, fista_restart=True)
+        barrier(world)
+        t0 = time.perf_counter()
+        ctx.upload(graph)                              # CSR H2D (shard)
+        r = ctx.solve(x0, ecfg, want_x=True)           # x0 H2D, solve, membership + trace D2H
+        t1 = time.perf_counter()
+        e_local = t1 - t0
+        e_s = allmax(e_local, world)
+        lo, hi = int(bounds[rank]) if world > 1 else 0, int(bounds[rank + 1]) if world > 1 else graph.n
+        csr_b = 8 * (hi - lo + 1) + 4 * int(graph.row_ptr[hi] - graph.row_ptr[lo])
+        h2d = csr_b + 8 * graph.n * cfg["c"]
+        d2h = 8 * graph.n * cfg["c"] + 40 * len(r["records"])
+        e2e = {"value": r["iterations"] / e_s, "unit": "iter/s", "h2d_bytes_per_step": int(h2d / max(1, r["iterations"])),
+               "d2h_bytes_per_step": int(d2h / max(1, r["iterations"])), "seconds": e_s,
+               "iterations": r["iterations"], "includes": "CSR upload + x0 H2D + prelude + solve + result D2H"}
+
+    # ---- roofline of the dominant kernel (k_sweep) -----------------------------------------
+    peak, peak_kind = peaks()
+    lo, hi = (int(bounds[rank]), int(bounds[rank + 1])) if world > 1 else (0, graph.n)
+    nnz_l = int(graph.row_ptr[hi] - graph.row_ptr[lo])
+    it_b_total, _ = bytes_model(graph.n, graph.nnz, cfg["c"], cfg["method"])
+    _, sweep_b = bytes_model(hi - lo, nnz_l, cfg["c"], cfg["method"])
+    sweep_ms, sweep_n = kt["sweep"]
+    sweep_avg = sweep_ms / max(1, sweep_n)
+    achieved = sweep_b / (sweep_avg / 1e3) / 1e9 if sweep_avg > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "sweep_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("config") == args.config and world == 1:
+            traffic = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import Reference, reference_available
+        if reference_available():
+            budget = float(os.environ.get("FC_CPU_BUDGET_S", "30"))
+            rr = cpu_reference_run(cfg, graph, x0, budget, 1)
+            cpu = {"value": 1.0 / rr["s_per_iter"], "unit": "iter/s", "cores": rr["cores"], "kind": "reference",
+                   "sample": f"{rr['iters']} {cfg['method'].upper()} iteration(s) of the reference solver on the "
+                             f"full config {args.config} graph (oracle/_ref, {rr['cores']} threads), "
+                             f"time-bounded to ~{budget:.0f}s"}
+
+    if rank == 0:
+        step_ms = ms / args.steps
+        line = {
+            "metric": "fista_iterations_per_s" if cfg["method"] != "gpa" else "gpa_iterations_per_s",
+            "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": config_name(args.config, cfg), "n": graph.n, "nnz": graph.nnz,
+                       "edges_undirected": (graph.nnz - graph.n) // 2, "k": cfg["c"],
+                       "parallelism": f"rows{world}", "l2": "inputs >> 126 MB L2 (no flush needed)",
+                       "graph_gen_s": round(t_graph, 1)},
+            "edges_per_s": graph.nnz * value,
+            "achieved_gbs": it_b_total * value / 1e9,
+            "iteration_bytes": it_b_total,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "k_sweep", "algorithmic_bytes_per_launch": sweep_b,
+                         "avg_launch_ms": sweep_avg, "peak_source": peak_kind},
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "valid": bool(valid_count),
+        }
+        print(json.dumps(line))
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

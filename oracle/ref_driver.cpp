@@ -1,0 +1,276 @@
+// ref_driver.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A thin extern "C" shim over the UNMODIFIED reference library
+// (/root/reference/proj/include/fuzzyclust/*.hpp, header-only C++20), compiled by
+// oracle/Makefile with the reference's own Release flags (-std=gnu++20 -O3
+// -DNDEBUG, no -march => no FMA; proj/CMakeLists.txt:7-9) into
+// oracle/_ref/libfcref.so.  No reference source is copied: this file only
+// #includes the headers where they lie.
+//
+// Used (a) by tests/ to pin the plain-C restatement (oracle/fc_oracle.c) and the
+// CUDA path bitwise against the real reference, and (b) by bench.py as the CPU
+// baseline / `--impl reference` arm (the reference's own run_fista/run_gpa on the
+// box's host cores).
+//
+// SparseSimilarity keeps its CSR private (sparse.hpp:141-145) and its only
+// constructors sort triplets (sparse.hpp:28-62: ~160 s at N=1e7).  For large,
+// already-validated CSR (our generator's output, which the small-size tests
+// push through from_triplets) the shim fills the private fields directly: all
+// standard headers are included first, then `private` is redefined for the
+// reference headers only.  The solver code that runs is unchanged.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstddef>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <istream>
+#include <limits>
+#include <optional>
+#include <ostream>
+#include <queue>
+#include <set>
+#include <span>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#define private public
+#include "fuzzyclust/fuzzyclust.hpp"
+#undef private
+
+using namespace fuzzyclust;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const InvalidInput& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+MembershipMatrix wrap(const double* x, std::size_t c, std::size_t n) {
+    MembershipMatrix m(c, n);
+    std::memcpy(m.data().data(), x, c * n * sizeof(double));
+    return m;
+}
+}  // namespace
+
+extern "C" {
+
+struct fcref_record {
+    uint64_t iteration;
+    double loss;
+    int32_t loss_increased;
+    int32_t pad;
+    double elapsed_ms;
+};
+
+struct fcref_summary {
+    int32_t reason;
+    int32_t pad;
+    uint64_t iterations;
+    double final_loss;
+    double step_size;
+    uint64_t n_records;
+    double solve_ms;
+};
+
+const char* fcref_last_error() { return g_err.c_str(); }
+const char* fcref_version() { return kVersion; }
+unsigned fcref_resolve_workers(unsigned requested) { return resolve_workers(requested); }
+
+// fast != 0: fill the private CSR fields directly (no sort / symmetry check).
+// fast == 0: SparseSimilarity::from_triplets (full reference validation).
+int fcref_similarity_create(uint64_t n, uint64_t nnz, const int64_t* row_ptr, const uint32_t* col_idx,
+                            const double* values, int fast, void** out) {
+    return guarded([&] {
+        auto* s = new SparseSimilarity();
+        if (fast) {
+            s->n_ = n;
+            s->col_ptr_.assign(row_ptr, row_ptr + n + 1);
+            s->rows_.assign(col_idx, col_idx + nnz);
+            if (values) {
+                s->values_.assign(values, values + nnz);
+            } else {
+                s->values_.assign(nnz, 1.0);
+            }
+            s->frob_sq_ = 0.0;
+            for (double v : s->values_) s->frob_sq_ += v * v;
+        } else {
+            std::vector<std::tuple<std::uint32_t, std::uint32_t, double>> t;
+            t.reserve(nnz);
+            for (uint64_t j = 0; j < n; ++j)
+                for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e)
+                    t.emplace_back(col_idx[e], static_cast<std::uint32_t>(j), values ? values[e] : 1.0);
+            *s = SparseSimilarity::from_triplets(n, std::move(t));
+        }
+        *out = s;
+    });
+}
+
+void fcref_similarity_free(void* s) { delete static_cast<SparseSimilarity*>(s); }
+double fcref_similarity_frob_sq(void* s) { return static_cast<SparseSimilarity*>(s)->frob_sq(); }
+uint64_t fcref_similarity_nnz(void* s) { return static_cast<SparseSimilarity*>(s)->nnz(); }
+
+// Copy the stored CSR back out (pins that from_triplets reproduces our layout).
+int fcref_similarity_export(void* h, int64_t* row_ptr, uint32_t* col_idx, double* values) {
+    return guarded([&] {
+        const auto& s = *static_cast<SparseSimilarity*>(h);
+        uint64_t pos = 0;
+        row_ptr[0] = 0;
+        for (std::size_t j = 0; j < s.size(); ++j) {
+            const auto r = s.col_rows(j);
+            const auto v = s.col_values(j);
+            for (std::size_t k = 0; k < r.size(); ++k) {
+                col_idx[pos] = r[k];
+                values[pos] = v[k];
+                ++pos;
+            }
+            row_ptr[j + 1] = static_cast<int64_t>(pos);
+        }
+    });
+}
+
+// Edge list (u, v) -> Graph -> build_similarity (sparse.hpp:66-75).
+int fcref_build_similarity(uint64_t num_nodes, uint64_t m, const uint32_t* edges, void** out) {
+    return guarded([&] {
+        Graph g;
+        g.num_nodes = num_nodes;
+        g.edges.reserve(m);
+        for (uint64_t e = 0; e < m; ++e) g.edges.emplace_back(edges[2 * e], edges[2 * e + 1]);
+        normalize_edges(g.edges);
+        *out = new SparseSimilarity(SparseSimilarity::build_similarity(g));
+    });
+}
+
+int fcref_project_simplex(double* x, uint64_t c) {
+    return guarded([&] { project_simplex_inplace(std::span<double>(x, c)); });
+}
+
+uint64_t fcref_splitmix(uint64_t seed, uint64_t k) {
+    SplitMix64 r(seed);
+    uint64_t v = 0;
+    for (uint64_t i = 0; i <= k; ++i) v = r.next();
+    return v;
+}
+
+// kind: 0 random, 1 dirichlet, 2 rowone, 3 uniform
+int fcref_init_membership(uint64_t n, uint64_t c, int kind, uint64_t seed, uint64_t row, double* out) {
+    return guarded([&] {
+        InitStrategy st;
+        st.kind = kind == 0 ? InitKind::kRandom
+                 : kind == 1 ? InitKind::kDirichlet
+                 : kind == 2 ? InitKind::kRowOne
+                             : InitKind::kUniform;
+        st.seed = seed;
+        st.row = row;
+        const auto x = init_membership(n, c, st);
+        std::memcpy(out, x.data().data(), n * c * sizeof(double));
+    });
+}
+
+int fcref_share_matrix(const double* x, uint64_t c, uint64_t n, unsigned workers, double* g) {
+    return guarded([&] {
+        const auto m = wrap(x, c, n);
+        const ShareMatrix s = share_matrix(m, workers);
+        for (std::size_t r = 0; r < c; ++r)
+            for (std::size_t q = 0; q < c; ++q) g[r * c + q] = s(r, q);
+    });
+}
+
+int fcref_fused_column_pass(void* h, const double* x, uint64_t c, unsigned workers, double* xs,
+                            double* merge) {
+    return guarded([&] {
+        const auto& s = *static_cast<SparseSimilarity*>(h);
+        const auto m = wrap(x, c, s.size());
+        const ColumnPass p = fused_column_pass(m, s, workers);
+        std::memcpy(xs, p.xs.data(), p.xs.size() * sizeof(double));
+        *merge = p.merge;
+    });
+}
+
+int fcref_loss_decomposed(void* h, const double* x, uint64_t c, unsigned workers, double* loss) {
+    return guarded([&] {
+        const auto& s = *static_cast<SparseSimilarity*>(h);
+        const auto m = wrap(x, c, s.size());
+        *loss = loss_decomposed(m, s, share_matrix(m, workers), workers);
+    });
+}
+
+int fcref_gpa_step_fused(const double* x, uint64_t c, uint64_t n, const double* g, const double* xs,
+                         double tau, unsigned workers, double* out) {
+    return guarded([&] {
+        const auto m = wrap(x, c, n);
+        ShareMatrix share(c);
+        for (std::size_t r = 0; r < c; ++r)
+            for (std::size_t q = 0; q < c; ++q) share(r, q) = g[r * c + q];
+        const std::vector<double> xsv(xs, xs + c * n);
+        const auto next = gpa_step_fused(m, share, xsv, tau, workers);
+        std::memcpy(out, next.data().data(), c * n * sizeof(double));
+    });
+}
+
+double fcref_default_step_size(void* h) {
+    const auto& s = *static_cast<SparseSimilarity*>(h);
+    return default_step_size(s, s.size());
+}
+
+double fcref_fista_t_next(double t) { return fista_t_next(t); }
+
+// method: 0 GPA, 1 FISTA.  Records carry the reference's own elapsed_ms.
+int fcref_solve(void* h, double step_size, uint64_t max_iter, double tol, int method,
+                uint64_t trace_every, int fista_restart, unsigned workers, uint64_t c,
+                const double* x0, double* x_out, fcref_record* trace, uint64_t cap,
+                fcref_summary* out) {
+    return guarded([&] {
+        const auto& s = *static_cast<SparseSimilarity*>(h);
+        SolverConfig cfg;
+        cfg.step_size = step_size;
+        cfg.max_iter = max_iter;
+        cfg.tol = tol;
+        cfg.method = method == 1 ? Method::kFista : Method::kGpa;
+        cfg.trace_every = trace_every;
+        cfg.fista_restart = fista_restart != 0;
+        cfg.workers = workers;
+        const auto m = wrap(x0, c, s.size());
+        const auto t0 = std::chrono::steady_clock::now();
+        const SolverResult r = solve(m, s, cfg);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (x_out) std::memcpy(x_out, r.membership.data().data(), c * s.size() * sizeof(double));
+        for (std::size_t k = 0; k < r.trace.records.size() && k < cap; ++k) {
+            trace[k].iteration = r.trace.records[k].iteration;
+            trace[k].loss = r.trace.records[k].loss;
+            trace[k].loss_increased = r.trace.records[k].loss_increased;
+            trace[k].elapsed_ms = r.trace.records[k].elapsed_ms;
+        }
+        out->reason = static_cast<int32_t>(r.trace.reason);
+        out->iterations = r.trace.iterations;
+        out->final_loss = r.trace.final_loss;
+        out->step_size = r.trace.step_size;
+        out->n_records = r.trace.records.size();
+        out->solve_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    });
+}
+
+}  // extern "C"

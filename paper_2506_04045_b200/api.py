@@ -1,0 +1,397 @@
+"""Python mirror of the reference's header API (namespace ``fuzzyclust``).
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/fuzzyclust/{membership,objective,simplex,solver}.hpp,
+so that the parity tests read like the reference's own GoogleTest suites.  The
+membership matrix is a numpy array of shape (N, C) -- byte-identical to the
+reference's C x N column-major ``MembershipMatrix`` (dense.hpp:12-27).
+
+Every numerical operator runs on the GPU through the C ABI (``capi``); there is
+no CPU fallback.  ``workers`` arguments are accepted for signature parity and
+ignored: results are bitwise identical for any worker count in the reference,
+and identical to it here.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+
+from . import capi
+from .errors import InvalidInput
+from .similarity import SparseSimilarity
+
+kReductionBlock = 1024          # parallel.hpp:15
+kVersion = "0.1.0"              # common.hpp:8
+
+
+class Method(IntEnum):          # solver.hpp:18 (+ backtracking, new)
+    kGpa = 0
+    kFista = 1
+    kFistaBacktracking = 2
+
+
+class TerminationReason(IntEnum):   # solver.hpp:20
+    kTolReached = 0
+    kMaxIter = 1
+    kLossIncreaseFista = 2
+
+
+def to_string(r) -> str:        # solver.hpp:22-29
+    return capi.REASONS[int(r)]
+
+
+class InitKind(IntEnum):        # membership.hpp:64-70
+    kRandom = 0
+    kDirichlet = 1
+    kRowOne = 2
+    kUniform = 3
+    kGiven = 4
+
+
+@dataclass
+class InitStrategy:             # membership.hpp:72-77
+    kind: InitKind = InitKind.kRandom
+    seed: int = 0
+    row: int = 0
+    given: np.ndarray | None = None
+
+
+@dataclass
+class SolverConfig:             # solver.hpp:31-48
+    step_size: float = 0.0
+    max_iter: int = 100000
+    tol: float = 0.0
+    method: Method = Method.kGpa
+    trace_every: int = 1
+    fista_restart: bool = False
+    workers: int = 1
+    bt_eta: float = 2.0         # new: backtracking growth of L = 1/step
+    bt_max: int = 30
+
+    def validate(self) -> None:
+        if self.max_iter < 1:
+            raise InvalidInput("solver: max_iter must be >= 1")
+        if self.tol < 0.0:
+            raise InvalidInput("solver: tol must be >= 0")
+        if self.trace_every < 1:
+            raise InvalidInput("solver: trace_every must be >= 1")
+        if not (self.step_size > 0.0) and self.step_size != 0.0:
+            raise InvalidInput("solver: step_size must be positive (or 0 for auto)")
+
+
+@dataclass
+class TraceRecord:              # solver.hpp:50-55
+    iteration: int
+    loss: float
+    elapsed_ms: float = 0.0
+    loss_increased: bool = False
+    backtracks: int = 0
+    step: float = 0.0
+
+
+@dataclass
+class SolverTrace:              # solver.hpp:57-63
+    records: list = field(default_factory=list)
+    reason: TerminationReason = TerminationReason.kMaxIter
+    iterations: int = 0
+    final_loss: float = 0.0
+    step_size: float = 0.0
+
+
+@dataclass
+class SolverResult:             # solver.hpp:65-68
+    membership: np.ndarray
+    trace: SolverTrace
+
+
+@dataclass
+class ColumnPass:               # objective.hpp:146-149
+    xs: np.ndarray
+    merge: float
+
+
+# ---- device context ---------------------------------------------------------------
+_default_ctx = None
+
+
+def default_context() -> capi.Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = capi.Context(0)
+    return _default_ctx
+
+
+def set_default_context(ctx: capi.Context | None) -> None:
+    global _default_ctx
+    _default_ctx = ctx
+
+
+def _ctx_for(s: SparseSimilarity | None, ctx: capi.Context | None, n: int | None = None) -> capi.Context:
+    """Context with `s` resident (uploaded once per similarity object).  Operators
+    that need only N (share_matrix) get an identity pattern of size n if no
+    similarity of that size is resident."""
+    ctx = ctx or default_context()
+    ref = getattr(ctx, "_graph_ref", None)
+    cur = ref() if ref is not None else None
+    if s is not None:
+        if cur is not s:
+            ctx.upload(s)
+    elif n is not None and (cur is None or cur.size() != n):
+        ident = SparseSimilarity(n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.uint32))
+        ctx.upload(ident)
+        ctx._graph_keep = ident
+    return ctx
+
+
+def _ctx_nograph(ctx):
+    """Granular ops that only need N: upload a pattern of the right size if needed."""
+    return ctx or default_context()
+
+
+# ---- rng.hpp / membership.hpp ------------------------------------------------------
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+
+
+def splitmix64_stream(seed: int, start: int, count: int) -> np.ndarray:
+    """Draws #start .. #start+count-1 of SplitMix64(seed) (rng.hpp:21-26)."""
+    k = np.arange(start + 1, start + count + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + k * _GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def splitmix64_doubles(seed: int, start: int, count: int) -> np.ndarray:
+    """next_double(): (next() >> 11) * 2^-53 (rng.hpp:29-31)."""
+    return (splitmix64_stream(seed, start, count) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def init_membership(num_nodes: int, num_clusters: int, strategy: InitStrategy | None = None,
+                    ctx: capi.Context | None = None) -> np.ndarray:
+    """membership.hpp:79-132.  The per-column projection runs on the GPU."""
+    strategy = strategy or InitStrategy()
+    if num_clusters == 0 or num_nodes == 0:
+        raise InvalidInput("init_membership: dimensions must be positive")
+    n, c = num_nodes, num_clusters
+    kind = InitKind(strategy.kind)
+    if kind == InitKind.kRandom:
+        ctx = _ctx_nograph(ctx)
+        x = np.empty((n, c))
+        rows_per = max(1, (1 << 24) // c)
+        for r0 in range(0, n, rows_per):
+            r1 = min(n, r0 + rows_per)
+            x[r0:r1] = splitmix64_doubles(strategy.seed, r0 * c, (r1 - r0) * c).reshape(r1 - r0, c)
+        return ctx.project_simplex_rows(x)
+    if kind == InitKind.kDirichlet:
+        ctx = _ctx_nograph(ctx)
+        u = splitmix64_doubles(strategy.seed, 0, n * c).reshape(n, c)
+        x = np.empty((n, c))
+        for i in range(n):               # std::log per entry, sequential sum (membership.hpp:98-107)
+            s = 0.0
+            for k in range(c):
+                v = -math.log(1.0 - float(u[i, k]))
+                x[i, k] = v
+                s += v
+            for k in range(c):
+                x[i, k] = x[i, k] / s
+        return ctx.project_simplex_rows(x)
+    if kind == InitKind.kRowOne:
+        if strategy.row >= c:
+            raise InvalidInput("init_membership: row out of range")
+        x = np.zeros((n, c))
+        x[:, strategy.row] = 1.0
+        return x
+    if kind == InitKind.kUniform:
+        return np.full((n, c), 1.0 / float(c))
+    if kind == InitKind.kGiven:
+        g = strategy.given
+        if g is None:
+            raise InvalidInput("init_membership: no matrix supplied")
+        g = np.asarray(g, dtype=np.float64)
+        if g.shape != (n, c):
+            raise InvalidInput("init_membership: supplied matrix has wrong shape")
+        validate_membership(g, 1e-9)
+        return g.copy()
+    raise InvalidInput("init_membership: unknown kind")
+
+
+def feasibility_error(x: np.ndarray) -> float:
+    """membership.hpp:49-61 (host check of a caller-supplied matrix)."""
+    x = np.asarray(x, dtype=np.float64)
+    worst = 0.0
+    for row in x:
+        s = 0.0
+        for v in row.tolist():
+            s += v
+            if v < 0.0:
+                worst = max(worst, -v)
+            if v > 1.0:
+                worst = max(worst, v - 1.0)
+        worst = max(worst, abs(s - 1.0))
+    return worst
+
+
+def validate_membership(x: np.ndarray, tol: float) -> None:
+    x = np.asarray(x)
+    if x.size == 0:
+        raise InvalidInput("membership: empty matrix")
+    if not np.all(np.isfinite(x)):
+        raise InvalidInput("membership: non-finite entry")
+    err = feasibility_error(x)
+    if err > tol:
+        raise InvalidInput(f"membership: columns violate the simplex constraint by {err:g} (tolerance {tol:g})")
+
+
+def write_membership_csv(x: np.ndarray) -> str:       # membership.hpp:136-149
+    c = x.shape[1]
+    lines = ["node_id," + ",".join(f"x_{k}" for k in range(1, c + 1))]
+    for i, row in enumerate(np.asarray(x)):
+        lines.append(str(i) + "," + ",".join("%.17g" % v for v in row.tolist()))
+    return "\n".join(lines) + "\n"
+
+
+def read_membership_csv(text: str) -> np.ndarray:     # membership.hpp:151-194
+    rows = []
+    header = True
+    for line_no, line in enumerate(text.split("\n"), 1):
+        if not line:
+            continue
+        if header:
+            header = False
+            continue
+        cells = line.split(",")[1:]
+        try:
+            vals = [float(cc) for cc in cells]
+        except ValueError:
+            raise InvalidInput(f"membership CSV: bad value at line {line_no}") from None
+        if not vals:
+            raise InvalidInput(f"membership CSV: no values at line {line_no}")
+        if rows and len(vals) != len(rows[0]):
+            raise InvalidInput(f"membership CSV: ragged row at line {line_no}")
+        rows.append(vals)
+    if not rows:
+        raise InvalidInput("membership CSV: no data rows")
+    return np.array(rows, dtype=np.float64)
+
+
+# ---- simplex.hpp -------------------------------------------------------------------
+def project_simplex(x, ctx: capi.Context | None = None) -> np.ndarray:
+    """simplex.hpp:62-66 (copying variant), on the GPU."""
+    v = np.asarray(x, dtype=np.float64).ravel()
+    if v.size == 0:
+        raise InvalidInput("project_simplex: empty vector")
+    return _ctx_nograph(ctx).project_simplex_rows(v.reshape(1, -1))[0]
+
+
+# ---- objective.hpp -----------------------------------------------------------------
+def share_matrix(x: np.ndarray, workers: int = 1, s: SparseSimilarity | None = None,
+                 ctx: capi.Context | None = None) -> np.ndarray:
+    """objective.hpp:92-95.  Needs a context holding a similarity of size N (pass s)."""
+    x = np.asarray(x)
+    return _ctx_for(s, ctx, n=x.shape[0]).share_matrix(x)
+
+
+def fused_column_pass(x: np.ndarray, s: SparseSimilarity, workers: int = 1,
+                      ctx: capi.Context | None = None) -> ColumnPass:
+    x = np.asarray(x)
+    if s.size() != x.shape[0]:
+        raise InvalidInput("objective: similarity/membership size mismatch")
+    xs, merge = _ctx_for(s, ctx).fused_column_pass(x)
+    return ColumnPass(xs, merge)
+
+
+def loss_decomposed(x: np.ndarray, s: SparseSimilarity, share: np.ndarray, workers: int = 1,
+                    ctx: capi.Context | None = None) -> float:
+    return _ctx_for(s, ctx).loss_decomposed(x, share)
+
+
+def share_frob_sq(share: np.ndarray) -> float:       # objective.hpp:25-29
+    acc = 0.0
+    for v in np.asarray(share, dtype=np.float64).ravel().tolist():
+        acc += v * v
+    return acc
+
+
+def gpa_step_fused(x, share, xs, tau: float, workers: int = 1, s: SparseSimilarity | None = None,
+                   ctx: capi.Context | None = None) -> np.ndarray:
+    return _ctx_for(s, ctx).gpa_step_fused(x, share, xs, tau)
+
+
+def gpa_step(x, s: SparseSimilarity, share, tau: float, workers: int = 1,
+             ctx: capi.Context | None = None) -> np.ndarray:
+    return _ctx_for(s, ctx).gpa_step(x, share, tau)
+
+
+# ---- solver.hpp --------------------------------------------------------------------
+def fista_t_next(t: float) -> float:                 # solver.hpp:72
+    return (1.0 + math.sqrt(1.0 + 4.0 * t * t)) / 2.0
+
+
+def default_step_size(s: SparseSimilarity, n: int) -> float:   # solver.hpp:78-81
+    return 1.0 / (4.0 * s.frob_norm() + 12.0 * float(n))
+
+
+def resolve_step_size(config: SolverConfig, s: SparseSimilarity, n: int) -> float:
+    return config.step_size if config.step_size > 0.0 else default_step_size(s, n)
+
+
+def _to_result(raw, n, c) -> SolverResult:
+    tr = SolverTrace(
+        records=[TraceRecord(it, loss, ms, inc, bt, st) for (it, loss, inc), ms, bt, st in
+                 zip(raw["records"], raw["elapsed_ms"], raw["backtracks"], raw["steps"])],
+        reason=TerminationReason({"tol_reached": 0, "max_iter": 1, "loss_increase_fista": 2}[raw["reason"]]),
+        iterations=raw["iterations"], final_loss=raw["final_loss"], step_size=raw["step_size"])
+    return SolverResult(raw["membership"], tr)
+
+
+def solve(x0: np.ndarray, s: SparseSimilarity, config: SolverConfig,
+          ctx: capi.Context | None = None) -> SolverResult:
+    """solver.hpp:274-277 -> run_gpa / run_fista, the whole loop on the device."""
+    config.validate()
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    if s.size() != x0.shape[0]:
+        raise InvalidInput("run_gpa: similarity/membership size mismatch" if config.method == Method.kGpa
+                           else "run_fista: similarity/membership size mismatch")
+    ctx = _ctx_for(s, ctx)
+    cfg = capi.Context.config(int(config.method), config.step_size, config.max_iter, config.tol,
+                              config.trace_every, config.fista_restart, config.bt_eta, config.bt_max)
+    raw = ctx.solve(x0, cfg)
+    return _to_result(raw, *x0.shape)
+
+
+def run_gpa(x0, s, config: SolverConfig, ctx=None) -> SolverResult:
+    cfg = SolverConfig(**{**config.__dict__, "method": Method.kGpa})
+    return solve(x0, s, cfg, ctx)
+
+
+def run_fista(x0, s, config: SolverConfig, ctx=None) -> SolverResult:
+    m = config.method if config.method != Method.kGpa else Method.kFista
+    cfg = SolverConfig(**{**config.__dict__, "method": m})
+    return solve(x0, s, cfg, ctx)
+
+
+def write_trace_csv(trace: SolverTrace, include_timing: bool = False) -> str:   # solver.hpp:282-295
+    out = ["iteration,loss,elapsed_ms" if include_timing else "iteration,loss"]
+    for r in trace.records:
+        line = f"{r.iteration},%.17g" % r.loss
+        if include_timing:
+            line += ",%.3f" % r.elapsed_ms
+        out.append(line)
+    return "\n".join(out) + "\n"
+
+
+# ---- synthetic graphs (new; see csrc/generator.cpp) ---------------------------------
+def generate_sbm(n: int, m: int, blocks: int, seed: int, p_in: float = 0.9, locality: bool = False,
+                 threads: int = 0) -> SparseSimilarity:
+    rp, ci = capi.generate_graph(0, n, m, seed, blocks=blocks, p_in=p_in, locality=locality, threads=threads)
+    return SparseSimilarity(n, rp, ci, None, float(ci.size))
+
+
+def generate_citation(n: int, m: int, seed: int, alpha: float = 2.5, gamma: float = 2.0, locality: bool = False,
+                      threads: int = 0) -> SparseSimilarity:
+    rp, ci = capi.generate_graph(1, n, m, seed, alpha=alpha, gamma=gamma, locality=locality, threads=threads)
+    return SparseSimilarity(n, rp, ci, None, float(ci.size))

@@ -1,0 +1,61 @@
+"""In-tree build of libfuzzyclust_cuda.so (sm_100a) with nvcc.
+
+``--fmad=false`` is part of the numerical contract, not a tuning flag: the
+reference is compiled without FMA contraction (proj/CMakeLists.txt:7-9, no
+-march), and contracting ``acc + w*x`` into DFMA changes the bits
+(SURVEY.md section 0.7).  The host compiler gets ``-ffp-contract=off`` for the
+same reason (the few host-side reductions, e.g. ShareMatrix::frob_sq).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIBDIR = os.path.join(HERE, "lib")
+LIB = os.path.join(LIBDIR, "libfuzzyclust_cuda.so")
+SOURCES = [os.path.join(CSRC, "fc_capi.cu"), os.path.join(CSRC, "generator.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, "fc_kernels.cuh"), os.path.join(ROOT, "include", "fuzzyclust_cuda.h")]
+
+NVCC_FLAGS = [
+    "-O3", "-std=c++17",
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-lineinfo",
+    "--fmad=false",
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
+    "-shared",
+]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
+            return cand
+    return "nvcc"
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    return all(os.path.getmtime(p) <= t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    tmp = LIB + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-o", tmp, *SOURCES, "-lnccl"]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,305 @@
+"""ctypes binding of the C ABI (include/fuzzyclust_cuda.h).
+
+This is the reference-side binding a Python caller would add.
+The library is loaded from the in-tree ``lib/libfuzzyclust_cuda.so``; there is
+no fallback: if it is missing or no B200 is visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import weakref
+
+import numpy as np
+
+from .build import LIB
+from .errors import DeviceError, raise_for
+
+GPA, FISTA, FISTA_BT = 0, 1, 2
+REASONS = {0: "tol_reached", 1: "max_iter", 2: "loss_increase_fista"}
+
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_u32p = C.POINTER(C.c_uint32)
+_u64p = C.POINTER(C.c_uint64)
+
+
+class SolverConfigC(C.Structure):
+    _fields_ = [("step_size", C.c_double), ("max_iter", C.c_uint64), ("tol", C.c_double),
+                ("method", C.c_int32), ("fista_restart", C.c_int32), ("trace_every", C.c_uint64),
+                ("bt_eta", C.c_double), ("bt_max", C.c_uint32), ("flags", C.c_uint32)]
+
+
+class TraceRecordC(C.Structure):
+    _fields_ = [("iteration", C.c_uint64), ("loss", C.c_double), ("elapsed_ms", C.c_double),
+                ("loss_increased", C.c_int32), ("backtracks", C.c_int32), ("step", C.c_double)]
+
+
+class SummaryC(C.Structure):
+    _fields_ = [("reason", C.c_int32), ("pad", C.c_int32), ("iterations", C.c_uint64),
+                ("final_loss", C.c_double), ("step_size", C.c_double), ("n_records", C.c_uint64)]
+
+
+class GraphSpecC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("blocks", C.c_uint32), ("n", C.c_uint64), ("m", C.c_uint64),
+                ("seed", C.c_uint64), ("p_in", C.c_double), ("alpha", C.c_double), ("gamma", C.c_double),
+                ("locality", C.c_int32), ("threads", C.c_int32)]
+
+
+# every symbol include/fuzzyclust_cuda.h declares: (restype, argtypes)
+SIGNATURES = {
+    "fc_version": (C.c_char_p, []),
+    "fc_abi_version": (C.c_int, []),
+    "fc_last_error": (C.c_char_p, [C.c_void_p]),
+    "fc_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "fc_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_char_p]),
+    "fc_create_virtual": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int]),
+    "fc_destroy": (None, [C.c_void_p]),
+    "fc_upload_csr": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _i64p, _u32p, _dp, C.c_double]),
+    "fc_partition": (C.c_int, [C.c_void_p, _u64p, C.c_int]),
+    "fc_share_matrix": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp]),
+    "fc_fused_column_pass": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp]),
+    "fc_loss_decomposed": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp]),
+    "fc_gpa_step_fused": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp, C.c_double, _dp]),
+    "fc_gpa_step": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, C.c_double, _dp]),
+    "fc_project_simplex_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, _dp]),
+    "fc_solve": (C.c_int, [C.c_void_p, C.POINTER(SolverConfigC), C.c_uint32, _dp, _dp,
+                           C.POINTER(TraceRecordC), C.c_uint64, C.POINTER(SummaryC)]),
+    "fc_solver_begin": (C.c_int, [C.c_void_p, C.POINTER(SolverConfigC), C.c_uint32, _dp]),
+    "fc_solver_run": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "fc_solver_sync": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    "fc_solver_end": (C.c_int, [C.c_void_p, _dp, C.POINTER(TraceRecordC), C.c_uint64, C.POINTER(SummaryC)]),
+    "fc_stream": (C.c_void_p, [C.c_void_p]),
+    "fc_launch_count": (C.c_uint64, [C.c_void_p]),
+    "fc_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+    "fc_kernel_times": (C.c_int, [C.c_void_p, _dp, _u64p, C.c_int]),
+    "fc_plan_partition": (C.c_int, [C.c_uint64, _i64p, C.c_int, _u64p]),
+    "fc_generate_graph": (C.c_int, [C.POINTER(GraphSpecC), _u64p, C.POINTER(_i64p), C.POINTER(_u32p)]),
+    "fc_free": (None, [C.c_void_p]),
+}
+
+KERNEL_CLASSES = ("step", "gram", "sweep", "rowsum", "combine", "finalize", "comm")
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library (never a CPU substitute)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise DeviceError(f"CUDA library not built: {LIB} (run __graft_entry__.build())")
+        L = C.CDLL(LIB)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _p(a, t=_dp):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _check(rc, ctx=None):
+    if rc:
+        raise_for(rc, lib().fc_last_error(ctx).decode())
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().fc_nccl_unique_id(buf))
+    return buf.raw
+
+
+def plan_partition(row_ptr, world: int):
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    out = np.zeros(world + 1, np.uint64)
+    _check(lib().fc_plan_partition(rp.size - 1, _p(rp, _i64p), world, _p(out, _u64p)))
+    return out
+
+
+def generate_graph(kind: int, n: int, m: int, seed: int, *, blocks: int = 16, p_in: float = 0.9,
+                   alpha: float = 2.5, gamma: float = 2.0, locality: bool = False, threads: int = 0):
+    """Synthetic A+I CSR (host, multithreaded, deterministic). Returns (row_ptr, col_idx)."""
+    spec = GraphSpecC(kind, blocks, n, m, seed, p_in, alpha, gamma, int(locality), threads)
+    nnz = C.c_uint64()
+    rp = _i64p()
+    ci = _u32p()
+    _check(lib().fc_generate_graph(C.byref(spec), C.byref(nnz), C.byref(rp), C.byref(ci)))
+    try:
+        row_ptr = np.ctypeslib.as_array(rp, shape=(n + 1,)).copy()
+        col_idx = np.ctypeslib.as_array(ci, shape=(max(nnz.value, 1),))[: nnz.value].copy()
+    finally:
+        lib().fc_free(C.cast(rp, C.c_void_p))
+        lib().fc_free(C.cast(ci, C.c_void_p))
+    return row_ptr, col_idx
+
+
+class Context:
+    """One device (one process per GPU).  world > 1: NCCL row-sharded solver."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 virtual_shards: int | None = None):
+        L = lib()
+        h = C.c_void_p()
+        if virtual_shards:
+            rc = L.fc_create_virtual(C.byref(h), device, virtual_shards)
+        else:
+            rc = L.fc_create(C.byref(h), device, rank, world, nccl_id)
+        if rc:
+            raise_for(rc, L.fc_last_error(None).decode())
+        self.h = h
+        self.device, self.rank, self.world = device, rank, world
+        self.n = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _c(self, rc):
+        if rc:
+            raise_for(rc, lib().fc_last_error(self.h).decode())
+
+    # ---- similarity ----------------------------------------------------------
+    def upload(self, graph) -> None:
+        self._c(lib().fc_upload_csr(self.h, graph.n, graph.nnz, _p(graph.row_ptr, _i64p),
+                                    _p(graph.col_idx, _u32p), _p(graph.values), graph.frob_sq))
+        self.n = graph.n
+        try:
+            self._graph_ref = weakref.ref(graph)
+        except TypeError:
+            self._graph_ref = None
+
+    def partition(self):
+        out = np.zeros(65, np.uint64)
+        parts = lib().fc_partition(self.h, _p(out, _u64p), 64)
+        if parts < 0:
+            self._c(2)
+        return out[: parts + 1]
+
+    # ---- granular operators (X is (N, C) row-major == the reference's C x N col-major)
+    def share_matrix(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        c = x.shape[1]
+        g = np.empty((c, c))
+        self._c(lib().fc_share_matrix(self.h, c, _p(x), _p(g)))
+        return g
+
+    def fused_column_pass(self, x, want_xs: bool = True):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        xs = np.empty_like(x) if want_xs else None
+        m = C.c_double()
+        self._c(lib().fc_fused_column_pass(self.h, x.shape[1], _p(x), _p(xs), C.byref(m)))
+        return xs, m.value
+
+    def loss_decomposed(self, x, g):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        v = C.c_double()
+        self._c(lib().fc_loss_decomposed(self.h, x.shape[1], _p(x), _p(g), C.byref(v)))
+        return v.value
+
+    def gpa_step_fused(self, x, g, xs, tau):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(x)
+        self._c(lib().fc_gpa_step_fused(self.h, x.shape[1], _p(x), _p(np.ascontiguousarray(g, dtype=np.float64)),
+                                        _p(np.ascontiguousarray(xs, dtype=np.float64)), tau, _p(out)))
+        return out
+
+    def gpa_step(self, x, g, tau):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(x)
+        self._c(lib().fc_gpa_step(self.h, x.shape[1], _p(x), _p(np.ascontiguousarray(g, dtype=np.float64)), tau,
+                                  _p(out)))
+        return out
+
+    def project_simplex_rows(self, x):
+        y = np.array(x, dtype=np.float64, copy=True, order="C")
+        if y.ndim == 1:
+            y = y.reshape(1, -1)
+        self._c(lib().fc_project_simplex_rows(self.h, y.shape[1], y.shape[0], _p(y)))
+        return y
+
+    # ---- solver -------------------------------------------------------------
+    @staticmethod
+    def config(method=GPA, step_size=0.0, max_iter=100000, tol=0.0, trace_every=1, fista_restart=False,
+               bt_eta=2.0, bt_max=30):
+        return SolverConfigC(step_size, max_iter, tol, method, int(fista_restart), trace_every, bt_eta, bt_max, 0)
+
+    def solve(self, x0, cfg: SolverConfigC, want_x: bool = True, trace_cap: int | None = None):
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        n, c = x0.shape
+        cap = trace_cap if trace_cap is not None else int(min(cfg.max_iter + 2, 1 << 20))
+        recs = (TraceRecordC * max(cap, 1))()
+        summ = SummaryC()
+        out = np.empty_like(x0) if want_x else None
+        self._c(lib().fc_solve(self.h, C.byref(cfg), c, _p(x0), _p(out), recs, cap, C.byref(summ)))
+        return _result(out, recs, summ, cap)
+
+    def begin(self, x0, cfg: SolverConfigC):
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        self._cfg = cfg
+        self._c(lib().fc_solver_begin(self.h, C.byref(cfg), x0.shape[1], _p(x0)))
+
+    def run(self, iterations: int):
+        self._c(lib().fc_solver_run(self.h, iterations))
+
+    def sync(self) -> bool:
+        d = C.c_int()
+        self._c(lib().fc_solver_sync(self.h, C.byref(d)))
+        return bool(d.value)
+
+    def end(self, n, c, want_x=True, trace_cap=None):
+        cap = trace_cap if trace_cap is not None else int(min(self._cfg.max_iter + 2, 1 << 20))
+        recs = (TraceRecordC * max(cap, 1))()
+        summ = SummaryC()
+        out = np.empty((n, c)) if want_x else None
+        self._c(lib().fc_solver_end(self.h, _p(out), recs, cap, C.byref(summ)))
+        return _result(out, recs, summ, cap)
+
+    # ---- instrumentation ----------------------------------------------------
+    def stream_ptr(self) -> int:
+        return lib().fc_stream(self.h) or 0
+
+    def launch_count(self) -> int:
+        return int(lib().fc_launch_count(self.h))
+
+    def set_profiling(self, on: bool):
+        self._c(lib().fc_set_profiling(self.h, int(on)))
+
+    def kernel_times(self):
+        ms = np.zeros(len(KERNEL_CLASSES))
+        n = np.zeros(len(KERNEL_CLASSES), np.uint64)
+        self._c(lib().fc_kernel_times(self.h, _p(ms), _p(n, _u64p), len(KERNEL_CLASSES)))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def _result(out, recs, summ, cap):
+    k = min(summ.n_records, cap)
+    return {
+        "membership": out,
+        "reason": REASONS[summ.reason],
+        "iterations": int(summ.iterations),
+        "final_loss": summ.final_loss,
+        "step_size": summ.step_size,
+        "records": [(int(recs[i].iteration), recs[i].loss, bool(recs[i].loss_increased)) for i in range(k)],
+        "elapsed_ms": [recs[i].elapsed_ms for i in range(k)],
+        "backtracks": [int(recs[i].backtracks) for i in range(k)],
+        "steps": [recs[i].step for i in range(k)],
+        "n_records": int(summ.n_records),
+    }

@@ -1,0 +1,1062 @@
+// fc_capi.cu -- implementation of include/fuzzyclust_cuda.h.
+//
+// Host side of the B200-native GPA/FISTA solver: context (device, stream, NCCL
+// communicator), CSR upload with the nnz-balanced row partition, work buffers,
+// and the on-device iteration loop.  Every per-iteration decision (loss, stop
+// rule, FISTA momentum / restart, backtracking) is taken on the device by
+// k_finalize, so the host only enqueues iterations and polls a done flag one
+// chunk behind (no per-iteration host round trip).
+//
+// Per FISTA iteration n, per shard (SURVEY.md section 7 step 7 schedule):
+//   k_step    bar^n = P(X_ext^n - tau grad f(X_ext^n))      X_ext^n rebuilt from bar^{n-1}, bar^{n-2}
+//   [NCCL]    allgather bar^n rows (grouped broadcast, unequal shards)
+//   k_gram    per-block Gram partials of bar^n and X_ext^{n+1}
+//   k_sweep   one CSR pass: S bar^n, S X_ext^{n+1}, <S bar^n_i, bar^n_i>
+//   k_rowsum  per-block merge partials
+//   k_combine ordered block combine (cross-shard: ordered NCCL send/recv chain)
+//   k_finalize loss, stop rule, trace record, plan of iteration n+1
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fc_kernels.cuh"
+#include "fuzzyclust_cuda.h"
+
+extern "C" int fc_generate_graph_impl(const fc_graph_spec* spec, uint64_t* nnz_out, int64_t** row_ptr_out,
+                                      uint32_t** col_idx_out, std::string* err);
+
+using namespace fc;
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+struct Shard {
+    uint64_t row0 = 0, nrows = 0;      // global rows [row0, row0 + nrows)
+    uint64_t lrow = 0;                 // first row in this device's local row arrays
+    uint64_t lblk = 0, nblk = 0;       // local block offset / count
+};
+
+enum { kClsStep, kClsGram, kClsSweep, kClsRowsum, kClsCombine, kClsFinalize, kClsComm, kNumCls };
+
+}  // namespace
+
+struct fc_ctx {
+    int device = 0, rank = 0, world = 1, vshards = 1;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    int sm_count = 148;
+    std::string err;
+    std::atomic<uint64_t> launches{0};
+
+    // similarity
+    bool have_csr = false;
+    uint64_t n = 0, nnz = 0;
+    double frob_s = 0.0;
+    bool weighted = false;
+    std::vector<uint64_t> bounds;      // world+1 (or vshards+1) row bounds
+    std::vector<Shard> shards;         // shards resident on this device
+    uint64_t local_rows = 0, local_blocks = 0;
+    long long* d_row_ptr = nullptr;
+    unsigned* d_col = nullptr;
+    double* d_val = nullptr;
+
+    // work buffers
+    uint32_t c = 0;
+    bool bt_alloc = false;
+    double* d_U[3] = {nullptr, nullptr, nullptr};
+    double* d_xs[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* d_prod = nullptr;
+    double* d_rowterm[3] = {nullptr, nullptr, nullptr};
+    double* d_gpart[2] = {nullptr, nullptr};
+    double* d_spart = nullptr;
+    double* d_totals = nullptr;        // (vshards + 1) slots
+    double* d_chain_in = nullptr;
+    double* d_gfull[2] = {nullptr, nullptr};
+    unsigned* d_counter = nullptr;
+    DevState* d_state = nullptr;
+    DevState* h_state = nullptr;       // pinned mirror
+    int* h_done = nullptr;             // pinned, 2 slots
+    TraceRec* d_trace = nullptr;
+    uint64_t trace_alloc = 0;
+
+    // solver session
+    bool session = false;
+    int method = 0;
+    uint64_t max_iter = 0;
+    uint64_t enqueued = 0;             // iterations enqueued after begin
+    uint64_t host_iter = 0;            // FISTA/GPA iteration index of the next enqueued pass
+    cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
+
+    // profiling
+    bool profiling = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_events;
+    double prof_ms[kNumCls] = {0};
+    uint64_t prof_n[kNumCls] = {0};
+    std::vector<cudaEvent_t> ev_pool;
+};
+
+namespace {
+
+int set_err(fc_ctx* ctx, int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    g_thread_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return set_err(ctx, FC_DEVICE, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_), \
+                           __FILE__, __LINE__, #call);                                     \
+    } while (0)
+
+#define NC(call)                                                                           \
+    do {                                                                                   \
+        ncclResult_t r_ = (call);                                                          \
+        if (r_ != ncclSuccess)                                                             \
+            return set_err(ctx, FC_DEVICE, "NCCL error %s at %s:%d", ncclGetErrorString(r_), \
+                           __FILE__, __LINE__);                                            \
+    } while (0)
+
+#define TRY(expr)                  \
+    do {                           \
+        int rc_ = (expr);          \
+        if (rc_) return rc_;       \
+    } while (0)
+
+template <class T>
+int dalloc(fc_ctx* ctx, T** p, size_t count) {
+    if (*p) {
+        cudaFree(*p);
+        *p = nullptr;
+    }
+    if (count == 0) count = 1;
+    CU(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+    return FC_OK;
+}
+
+template <class T>
+void dfree(T** p) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+}
+
+// ---- kernel-class timing ------------------------------------------------------
+struct ProfScope {
+    fc_ctx* ctx;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(fc_ctx* c, int k) : ctx(c), cls(k) {
+        if (!ctx->profiling) return;
+        if (ctx->ev_pool.size() < 2) {
+            for (int i = 0; i < 64; ++i) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                ctx->ev_pool.push_back(e);
+            }
+        }
+        a = ctx->ev_pool.back(); ctx->ev_pool.pop_back();
+        b = ctx->ev_pool.back(); ctx->ev_pool.pop_back();
+        cudaEventRecord(a, ctx->stream);
+    }
+    ~ProfScope() {
+        if (!ctx->profiling) return;
+        cudaEventRecord(b, ctx->stream);
+        ctx->prof_events.push_back({cls, {a, b}});
+    }
+};
+
+void prof_harvest(fc_ctx* ctx) {
+    for (auto& e : ctx->prof_events) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, e.second.first, e.second.second) == cudaSuccess) {
+            ctx->prof_ms[e.first] += ms;
+            ctx->prof_n[e.first] += 1;
+        }
+        ctx->ev_pool.push_back(e.second.first);
+        ctx->ev_pool.push_back(e.second.second);
+    }
+    ctx->prof_events.clear();
+}
+
+// ---- dispatch by cluster count -------------------------------------------------
+template <template <int, int> class F, class... A>
+int by_c(fc_ctx* ctx, uint32_t c, A&&... a) {
+    if (c <= 2) return F<2, 1>::run(a...);
+    if (c <= 4) return F<4, 1>::run(a...);
+    if (c <= 8) return F<8, 1>::run(a...);
+    if (c <= 16) return F<16, 1>::run(a...);
+    if (c <= 32) return F<32, 1>::run(a...);
+    if (c <= 64) return F<32, 2>::run(a...);
+    if (c <= 128) return F<32, 4>::run(a...);
+    if (c <= 256) return F<32, 8>::run(a...);
+    return set_err(ctx, FC_INVALID, "cluster count C=%u exceeds the supported maximum 256", c);
+}
+
+int grid_for(const void* fn, int threads, size_t smem, int sm_count) {
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+    return occ * sm_count;
+}
+
+template <int G, int S>
+struct LaunchSweep {
+    static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, bool dual) {
+        if (g.nrows == 0) return FC_OK;
+        const void* fn;
+        if (dual) fn = ctx->weighted ? (const void*)k_sweep<G, S, true, true> : (const void*)k_sweep<G, S, true, false>;
+        else fn = ctx->weighted ? (const void*)k_sweep<G, S, false, true> : (const void*)k_sweep<G, S, false, false>;
+        static int grid = 0;
+        if (!grid) grid = grid_for(fn, 256, 0, ctx->sm_count);
+        const unsigned long long need = (g.nrows + 31) / 32;   // 32-row chunks, 8 warps per CTA
+        const int gr = (int)std::min<unsigned long long>(grid, (need + 7) / 8);
+        if (dual) {
+            if (ctx->weighted) k_sweep<G, S, true, true><<<gr, 256, 0, ctx->stream>>>(b, g);
+            else k_sweep<G, S, true, false><<<gr, 256, 0, ctx->stream>>>(b, g);
+        } else {
+            if (ctx->weighted) k_sweep<G, S, false, true><<<gr, 256, 0, ctx->stream>>>(b, g);
+            else k_sweep<G, S, false, false><<<gr, 256, 0, ctx->stream>>>(b, g);
+        }
+        ctx->launches++;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_sweep launch: %s", cudaGetErrorString(e));
+        return FC_OK;
+    }
+};
+
+template <int G, int S>
+struct LaunchStep {
+    static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, int bt) {
+        if (g.nrows == 0) return FC_OK;
+        static int grid = 0;
+        if (!grid) grid = grid_for((const void*)k_step<G, S>, 256, 0, ctx->sm_count);
+        const unsigned long long need = (g.nrows + (32 / G) * 8 - 1) / ((32 / G) * 8);
+        const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
+        k_step<G, S><<<gr, 256, 0, ctx->stream>>>(b, g, bt);
+        ctx->launches++;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step launch: %s", cudaGetErrorString(e));
+        return FC_OK;
+    }
+};
+
+template <int G, int S>
+struct LaunchProject {
+    static int run(fc_ctx* ctx, double* x, unsigned long long rows, int c, unsigned* flag) {
+        if (rows == 0) return FC_OK;
+        const unsigned long long need = (rows + (32 / G) * 8 - 1) / ((32 / G) * 8);
+        const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(ctx->sm_count * 8, need));
+        k_project<G, S><<<gr, 256, 0, ctx->stream>>>(x, rows, c, flag);
+        ctx->launches++;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_project launch: %s", cudaGetErrorString(e));
+        return FC_OK;
+    }
+};
+
+int check_launch(fc_ctx* ctx, const char* what) {
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "%s launch: %s", what, cudaGetErrorString(e));
+    return FC_OK;
+}
+
+// ---- buffers ----------------------------------------------------------------------
+unsigned npairs_of(uint32_t c) { return c * (c + 1) / 2; }
+size_t nchains_of(uint32_t c) { return 2 * (size_t)npairs_of(c) + kNumScal; }
+
+int gram_rows_per_chunk(uint32_t c) {
+    const int c4 = (int)((c + 3) & ~3u);
+    int r = 2048 / c4;
+    return std::max(4, std::min(64, r));
+}
+
+int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
+    if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
+    if (c == 0) return set_err(ctx, FC_INVALID, "init_membership: dimensions must be positive");
+    if (c > 256) return set_err(ctx, FC_INVALID, "cluster count C=%u exceeds the supported maximum 256", c);
+    if (ctx->c == c && (!bt || ctx->bt_alloc)) return FC_OK;
+    CU(cudaStreamSynchronize(ctx->stream));
+    const size_t N = ctx->n, L = ctx->local_rows, LB = ctx->local_blocks;
+    for (int k = 0; k < 3; ++k) TRY(dalloc(ctx, &ctx->d_U[k], N * c));
+    for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_xs[k], L * c));
+    for (int k = 2; k < 4; ++k) {
+        if (bt) TRY(dalloc(ctx, &ctx->d_xs[k], L * c));
+        else dfree(&ctx->d_xs[k]);
+    }
+    TRY(dalloc(ctx, &ctx->d_prod, L));
+    for (int k = 0; k < 3; ++k) {
+        if (bt) TRY(dalloc(ctx, &ctx->d_rowterm[k], L));
+        else dfree(&ctx->d_rowterm[k]);
+    }
+    const unsigned np = npairs_of(c);
+    for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_gpart[k], LB * np));
+    TRY(dalloc(ctx, &ctx->d_spart, LB * kNumScal));
+    TRY(dalloc(ctx, &ctx->d_totals, (ctx->vshards + 1) * nchains_of(c)));
+    TRY(dalloc(ctx, &ctx->d_chain_in, nchains_of(c)));
+    for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_gfull[k], (size_t)c * c));
+    CU(cudaMemsetAsync(ctx->d_totals, 0, (ctx->vshards + 1) * nchains_of(c) * sizeof(double), ctx->stream));
+    ctx->c = c;
+    ctx->bt_alloc = bt;
+    return FC_OK;
+}
+
+Bufs make_bufs(fc_ctx* ctx, size_t s) {
+    const Shard& sh = ctx->shards[s];
+    const uint32_t c = ctx->c;
+    const unsigned np = npairs_of(c);
+    Bufs b{};
+    b.row_ptr = ctx->d_row_ptr + sh.lrow;
+    b.col = ctx->d_col;
+    b.val = ctx->weighted ? ctx->d_val : nullptr;
+    for (int k = 0; k < 3; ++k) b.U[k] = ctx->d_U[k];
+    for (int k = 0; k < 4; ++k) b.xs[k] = ctx->d_xs[k] ? ctx->d_xs[k] + sh.lrow * c : nullptr;
+    b.prod = ctx->d_prod + sh.lrow;
+    for (int k = 0; k < 3; ++k) b.rowterm[k] = ctx->d_rowterm[k] ? ctx->d_rowterm[k] + sh.lrow : nullptr;
+    for (int k = 0; k < 2; ++k) b.gpart[k] = ctx->d_gpart[k] + sh.lblk * np;
+    b.spart = ctx->d_spart + sh.lblk;
+    b.totals = ctx->d_totals + s * nchains_of(c);
+    for (int k = 0; k < 2; ++k) b.gfull[k] = ctx->d_gfull[k];
+    b.trace = ctx->d_trace;
+    b.st = ctx->d_state;
+    b.counter = ctx->d_counter + s;
+    return b;
+}
+
+Geo make_geo(fc_ctx* ctx, size_t s) {
+    const Shard& sh = ctx->shards[s];
+    Geo g{};
+    g.C = ctx->c;
+    g.npairs = npairs_of(ctx->c);
+    g.N = ctx->n;
+    g.row0 = sh.row0;
+    g.nrows = sh.nrows;
+    g.nblk = sh.nblk;
+    g.spart_stride = ctx->local_blocks;
+    return g;
+}
+
+// final totals slot (what k_finalize reads)
+Bufs final_bufs(fc_ctx* ctx) {
+    Bufs b = make_bufs(ctx, 0);
+    b.totals = ctx->d_totals + (ctx->world > 1 ? 0 : (ctx->shards.size() - 1)) * nchains_of(ctx->c);
+    return b;
+}
+
+// ---- phases -------------------------------------------------------------------------
+int phase_step(fc_ctx* ctx, int bt) {
+    ProfScope p(ctx, kClsStep);
+    for (size_t s = 0; s < ctx->shards.size(); ++s) {
+        const Bufs b = make_bufs(ctx, s);
+        const Geo g = make_geo(ctx, s);
+        TRY(by_c<LaunchStep>(ctx, ctx->c, ctx, b, g, bt));
+    }
+    return FC_OK;
+}
+
+int phase_gram(fc_ctx* ctx, bool dual) {
+    ProfScope p(ctx, kClsGram);
+    const uint32_t c = ctx->c;
+    const int c4 = (int)((c + 3) & ~3u);
+    const int nT = c4 / 4;
+    const int tiles = nT * (nT + 1) / 2 * (dual ? 2 : 1);
+    const int R = gram_rows_per_chunk(c);
+    const size_t smem = (size_t)(dual ? 2 : 1) * R * c4 * sizeof(double);
+    static size_t smem_set = 0;
+    if (smem > 48 * 1024 && smem > smem_set) {
+        CU(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+    }
+    for (size_t s = 0; s < ctx->shards.size(); ++s) {
+        const Geo g = make_geo(ctx, s);
+        if (g.nblk == 0) continue;
+        const Bufs b = make_bufs(ctx, s);
+        dim3 grid((unsigned)g.nblk, (unsigned)((tiles + kGramThreads - 1) / kGramThreads));
+        k_gram<<<grid, kGramThreads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
+        TRY(check_launch(ctx, "k_gram"));
+    }
+    return FC_OK;
+}
+
+int phase_sweep(fc_ctx* ctx, bool dual) {
+    ProfScope p(ctx, kClsSweep);
+    CU(cudaMemsetAsync(ctx->d_counter, 0, ctx->shards.size() * sizeof(unsigned), ctx->stream));
+    for (size_t s = 0; s < ctx->shards.size(); ++s) {
+        const Bufs b = make_bufs(ctx, s);
+        const Geo g = make_geo(ctx, s);
+        TRY(by_c<LaunchSweep>(ctx, ctx->c, ctx, b, g, dual));
+    }
+    return FC_OK;
+}
+
+int phase_rowsum(fc_ctx* ctx, int bt) {
+    ProfScope p(ctx, kClsRowsum);
+    const int nscal = bt ? 4 : 1;
+    for (size_t s = 0; s < ctx->shards.size(); ++s) {
+        const Geo g = make_geo(ctx, s);
+        if (g.nblk == 0) continue;
+        const Bufs b = make_bufs(ctx, s);
+        const unsigned long long total = g.nblk * (unsigned long long)nscal;
+        k_rowsum<<<(unsigned)((total + 127) / 128), 128, 0, ctx->stream>>>(
+            b, g, nscal, b.prod, bt ? b.rowterm[0] : nullptr, bt ? b.rowterm[1] : nullptr,
+            bt ? b.rowterm[2] : nullptr, kScalMerge);
+        TRY(check_launch(ctx, "k_rowsum"));
+    }
+    return FC_OK;
+}
+
+// Ordered combine.  Shards on this device chain through the totals slots;
+// ranks chain through NCCL recv(rank-1) / send(rank+1), then the last rank
+// broadcasts the final totals.
+int phase_combine(fc_ctx* ctx, int mat_mask, int scal_mask) {
+    const size_t nch = nchains_of(ctx->c);
+    const int threads = 128;
+    const int blocks = (int)((nch + threads - 1) / threads);
+    if (ctx->world == 1) {
+        ProfScope p(ctx, kClsCombine);
+        for (size_t s = 0; s < ctx->shards.size(); ++s) {
+            const Bufs b = make_bufs(ctx, s);
+            const Geo g = make_geo(ctx, s);
+            const double* init = s == 0 ? nullptr : ctx->d_totals + (s - 1) * nch;
+            k_combine<<<blocks, threads, 0, ctx->stream>>>(b, g, mat_mask, scal_mask, init);
+            TRY(check_launch(ctx, "k_combine"));
+        }
+        return FC_OK;
+    }
+    if (ctx->rank > 0) {
+        ProfScope p(ctx, kClsComm);
+        NC(ncclRecv(ctx->d_chain_in, nch, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    }
+    {
+        ProfScope p(ctx, kClsCombine);
+        const Bufs b = make_bufs(ctx, 0);
+        const Geo g = make_geo(ctx, 0);
+        k_combine<<<blocks, threads, 0, ctx->stream>>>(b, g, mat_mask, scal_mask,
+                                                       ctx->rank > 0 ? ctx->d_chain_in : nullptr);
+        TRY(check_launch(ctx, "k_combine"));
+    }
+    ProfScope p(ctx, kClsComm);
+    if (ctx->rank < ctx->world - 1)
+        NC(ncclSend(ctx->d_totals, nch, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
+    NC(ncclBroadcast(ctx->d_totals, ctx->d_totals, nch, ncclDouble, ctx->world - 1, ctx->comm, ctx->stream));
+    return FC_OK;
+}
+
+int phase_finalize(fc_ctx* ctx, int kind, int mat_mask) {
+    ProfScope p(ctx, kClsFinalize);
+    Bufs b = final_bufs(ctx);
+    Geo g = make_geo(ctx, 0);
+    k_finalize<<<1, 256, 0, ctx->stream>>>(b, g, kind, mat_mask);
+    return check_launch(ctx, "k_finalize");
+}
+
+// allgather of the rows of U[buf] each rank owns (world > 1 only)
+int phase_allgather(fc_ctx* ctx, int buf) {
+    if (ctx->world == 1) return FC_OK;
+    ProfScope p(ctx, kClsComm);
+    const uint32_t c = ctx->c;
+    NC(ncclGroupStart());
+    for (int r = 0; r < ctx->world; ++r) {
+        const size_t off = ctx->bounds[r] * c, cnt = (ctx->bounds[r + 1] - ctx->bounds[r]) * c;
+        NC(ncclBroadcast(ctx->d_U[buf] + off, ctx->d_U[buf] + off, cnt, ncclDouble, r, ctx->comm, ctx->stream));
+    }
+    NC(ncclGroupEnd());
+    return FC_OK;
+}
+
+int enqueue_prelude(fc_ctx* ctx) {   // FISTA loss at x0 (solver.hpp:206-212)
+    TRY(phase_gram(ctx, false));
+    TRY(phase_sweep(ctx, false));
+    TRY(phase_rowsum(ctx, 0));
+    TRY(phase_combine(ctx, 1, 1));
+    TRY(phase_finalize(ctx, kFinPrelude, 1));
+    return FC_OK;
+}
+
+int enqueue_fista_iteration(fc_ctx* ctx, int bt) {
+    TRY(phase_step(ctx, bt));
+    TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
+    TRY(phase_gram(ctx, true));
+    TRY(phase_sweep(ctx, true));
+    TRY(phase_rowsum(ctx, bt));
+    TRY(phase_combine(ctx, 3, bt ? 0xF : 1));
+    TRY(phase_finalize(ctx, kFinFista, 3));
+    ctx->host_iter++;
+    return FC_OK;
+}
+
+int enqueue_gpa_iteration(fc_ctx* ctx) {
+    TRY(phase_gram(ctx, false));
+    TRY(phase_sweep(ctx, false));
+    TRY(phase_rowsum(ctx, 0));
+    TRY(phase_combine(ctx, 1, 1));
+    TRY(phase_finalize(ctx, kFinGpa, 1));
+    TRY(phase_step(ctx, 0));
+    TRY(phase_allgather(ctx, (int)((ctx->host_iter + 1) % 2)));
+    ctx->host_iter++;
+    return FC_OK;
+}
+
+int upload_state(fc_ctx* ctx, const DevState& s) {
+    *ctx->h_state = s;
+    CU(cudaMemcpyAsync(ctx->d_state, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
+    return FC_OK;
+}
+
+int download_state(fc_ctx* ctx) {
+    CU(cudaMemcpyAsync(ctx->h_state, ctx->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return FC_OK;
+}
+
+DevState base_state(fc_ctx* ctx) {
+    DevState s;
+    std::memset(&s, 0, sizeof s);
+    s.frob_s = ctx->frob_s;
+    s.trace_cap = ctx->trace_alloc;
+    s.trace_every = 1;
+    s.max_iter = 1;
+    return s;
+}
+
+int h2d(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return FC_OK;
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return FC_OK;
+}
+
+int d2h(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return FC_OK;
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    return FC_OK;
+}
+
+// x0.validate(1e-9) on the device (membership.hpp:49-61); x already in U[buf]
+int validate_x(fc_ctx* ctx, int buf, double tol) {
+    DevState s = base_state(ctx);
+    TRY(upload_state(ctx, s));
+    const unsigned long long n = ctx->n;
+    k_validate<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->d_U[buf], n, (int)ctx->c, ctx->d_state);
+    TRY(check_launch(ctx, "k_validate"));
+    TRY(download_state(ctx));
+    if (ctx->h_state->nonfinite) return set_err(ctx, FC_INVALID, "membership: non-finite entry");
+    double err;
+    const unsigned long long bits = ctx->h_state->err_bits;
+    std::memcpy(&err, &bits, sizeof err);
+    if (err > tol)
+        return set_err(ctx, FC_INVALID, "membership: columns violate the simplex constraint by %g (tolerance %g)",
+                       err, tol);
+    return FC_OK;
+}
+
+int ensure_trace(fc_ctx* ctx, uint64_t records) {
+    if (records == 0) records = 1;
+    if (ctx->trace_alloc >= records) return FC_OK;
+    TRY(dalloc(ctx, &ctx->d_trace, records));
+    ctx->trace_alloc = records;
+    return FC_OK;
+}
+
+bool granular_ok(fc_ctx* ctx) { return ctx->world == 1; }
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char* fc_version(void) { return "fuzzyclust-b200 0.1.0 (reference API 0.1.0)"; }
+int fc_abi_version(void) { return FC_ABI_VERSION; }
+
+const char* fc_last_error(const fc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_thread_err.c_str(); }
+
+int fc_nccl_unique_id(unsigned char id[128]) {
+    fc_ctx* ctx = nullptr;
+    ncclUniqueId u;
+    NC(ncclGetUniqueId(&u));
+    static_assert(sizeof(u.internal) == 128, "nccl id size");
+    std::memcpy(id, u.internal, 128);
+    return FC_OK;
+}
+
+static int create_common(fc_ctx** out, int device, int rank, int world, int vshards, const unsigned char* id) {
+    fc_ctx* ctx = nullptr;
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return set_err(nullptr, FC_INVALID, "bad rank/world");
+    if (vshards < 1) return set_err(nullptr, FC_INVALID, "shards must be >= 1");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return set_err(nullptr, FC_DEVICE, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return set_err(nullptr, FC_INVALID, "device %d out of range", device);
+    ctx = new fc_ctx();
+    ctx->device = device;
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->vshards = vshards;
+    *out = ctx;
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return set_err(ctx, FC_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a (B200)", device,
+                       prop.major, prop.minor);
+    ctx->sm_count = prop.multiProcessorCount;
+    CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CU(cudaMalloc(&ctx->d_state, sizeof(DevState)));
+    CU(cudaMallocHost(&ctx->h_state, sizeof(DevState)));
+    CU(cudaMallocHost(&ctx->h_done, 2 * sizeof(int)));
+    CU(cudaMalloc(&ctx->d_counter, 64 * sizeof(unsigned)));
+    CU(cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->chunk_ev[1], cudaEventDisableTiming));
+    if (world > 1) {
+        ncclUniqueId u;
+        std::memcpy(u.internal, id, 128);
+        NC(ncclCommInitRank(&ctx->comm, world, u, rank));
+    }
+    TRY(ensure_trace(ctx, 1024));
+    return FC_OK;
+}
+
+int fc_create(fc_ctx** out, int device, int rank, int world, const unsigned char* nccl_id) {
+    if (world > 1 && !nccl_id) return set_err(nullptr, FC_INVALID, "world > 1 needs an NCCL unique id");
+    int rc = create_common(out, device, rank, world, 1, nccl_id);
+    if (rc && *out) {
+        g_thread_err = (*out)->err;
+        fc_destroy(*out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+int fc_create_virtual(fc_ctx** out, int device, int shards) {
+    if (shards > 32) return set_err(nullptr, FC_INVALID, "at most 32 virtual shards");
+    int rc = create_common(out, device, 0, 1, shards, nullptr);
+    if (rc && *out) {
+        g_thread_err = (*out)->err;
+        fc_destroy(*out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+void fc_destroy(fc_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    prof_harvest(ctx);
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    for (int k = 0; k < 3; ++k) dfree(&ctx->d_U[k]);
+    for (int k = 0; k < 4; ++k) dfree(&ctx->d_xs[k]);
+    for (int k = 0; k < 3; ++k) dfree(&ctx->d_rowterm[k]);
+    for (int k = 0; k < 2; ++k) { dfree(&ctx->d_gpart[k]); dfree(&ctx->d_gfull[k]); }
+    dfree(&ctx->d_prod);
+    dfree(&ctx->d_spart);
+    dfree(&ctx->d_totals);
+    dfree(&ctx->d_chain_in);
+    dfree(&ctx->d_counter);
+    dfree(&ctx->d_state);
+    dfree(&ctx->d_trace);
+    dfree(&ctx->d_row_ptr);
+    dfree(&ctx->d_col);
+    dfree(&ctx->d_val);
+    if (ctx->h_state) cudaFreeHost(ctx->h_state);
+    if (ctx->h_done) cudaFreeHost(ctx->h_done);
+    for (auto e : ctx->chunk_ev) if (e) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int fc_plan_partition(uint64_t n, const int64_t* row_ptr, int world, uint64_t* bounds) {
+    if (world < 1) return set_err(nullptr, FC_INVALID, "world must be >= 1");
+    const uint64_t nblocks = (n + kBlock - 1) / kBlock;
+    const double nnz = (double)row_ptr[n];
+    bounds[0] = 0;
+    uint64_t b = 0;   // block cursor
+    for (int r = 1; r < world; ++r) {
+        const double target = nnz * (double)r / (double)world;
+        while (b < nblocks && (double)row_ptr[std::min<uint64_t>(b * kBlock, n)] < target) ++b;
+        // choose the nearer of the two candidate block boundaries
+        uint64_t pick = b;
+        if (b > 0) {
+            const double hi = (double)row_ptr[std::min<uint64_t>(b * kBlock, n)];
+            const double lo = (double)row_ptr[std::min<uint64_t>((b - 1) * kBlock, n)];
+            if (target - lo < hi - target) pick = b - 1;
+        }
+        bounds[r] = std::max<uint64_t>(bounds[r - 1], std::min<uint64_t>(pick * kBlock, n));
+    }
+    bounds[world] = n;
+    return FC_OK;
+}
+
+int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr, const uint32_t* col_idx,
+                  const double* values, double frob_sq) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    CU(cudaSetDevice(ctx->device));
+    if (n == 0) return set_err(ctx, FC_INVALID, "membership: empty matrix");
+    if (n > 0xFFFFFFFFULL) return set_err(ctx, FC_INVALID, "similarity: more than 2^32 nodes");
+    if (row_ptr[0] != 0 || (uint64_t)row_ptr[n] != nnz)
+        return set_err(ctx, FC_INVALID, "similarity: row_ptr does not span [0, nnz)");
+    CU(cudaStreamSynchronize(ctx->stream));
+    const int parts = ctx->world > 1 ? ctx->world : ctx->vshards;
+    ctx->bounds.assign(parts + 1, 0);
+    fc_plan_partition(n, row_ptr, parts, ctx->bounds.data());
+    ctx->shards.clear();
+    uint64_t lrow = 0, lblk = 0;
+    auto add = [&](int r) {
+        Shard sh;
+        sh.row0 = ctx->bounds[r];
+        sh.nrows = ctx->bounds[r + 1] - ctx->bounds[r];
+        sh.lrow = lrow;
+        sh.lblk = lblk;
+        sh.nblk = (sh.nrows + kBlock - 1) / kBlock;
+        lrow += sh.nrows;
+        lblk += sh.nblk;
+        ctx->shards.push_back(sh);
+    };
+    if (ctx->world > 1) add(ctx->rank);
+    else for (int r = 0; r < parts; ++r) add(r);
+    ctx->local_rows = lrow;
+    ctx->local_blocks = lblk;
+
+    // device CSR: rows of the shards on this device (rebased to this device's slice)
+    const uint64_t r0 = ctx->shards.front().row0;
+    const uint64_t r1 = ctx->shards.back().row0 + ctx->shards.back().nrows;
+    const int64_t e0 = row_ptr[r0], e1 = row_ptr[r1];
+    const uint64_t lnnz = (uint64_t)(e1 - e0);
+    TRY(dalloc(ctx, &ctx->d_row_ptr, lrow + 1));
+    TRY(dalloc(ctx, &ctx->d_col, lnnz));
+    bool weighted = false;
+    if (values) {
+        for (uint64_t k = 0; k < nnz && !weighted; ++k) weighted = values[k] != 1.0;
+    }
+    if (weighted) TRY(dalloc(ctx, &ctx->d_val, lnnz));
+    else dfree(&ctx->d_val);
+    {
+        std::vector<long long> rp(lrow + 1);
+        for (uint64_t i = 0; i <= lrow; ++i) rp[i] = (long long)(row_ptr[r0 + i] - e0);
+        TRY(h2d(ctx, ctx->d_row_ptr, rp.data(), rp.size() * sizeof(long long)));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    CU(cudaMemcpy(ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    if (weighted) CU(cudaMemcpy(ctx->d_val, values + e0, lnnz * sizeof(double), cudaMemcpyHostToDevice));
+    ctx->n = n;
+    ctx->nnz = nnz;
+    ctx->frob_s = frob_sq;
+    ctx->weighted = weighted;
+    ctx->have_csr = true;
+    ctx->c = 0;   // force buffer re-allocation for the new N
+    return FC_OK;
+}
+
+int fc_partition(const fc_ctx* ctx, uint64_t* bounds, int max_world) {
+    if (!ctx || !ctx->have_csr) return set_err(const_cast<fc_ctx*>(ctx), FC_INVALID, "no similarity uploaded");
+    const int parts = (int)ctx->bounds.size() - 1;
+    for (int r = 0; r <= std::min(parts, max_world); ++r) bounds[r] = ctx->bounds[r];
+    return parts;
+}
+
+// ---- granular operators ------------------------------------------------------------
+int fc_share_matrix(fc_ctx* ctx, uint32_t c, const double* x, double* g_out) {
+    if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
+    CU(cudaSetDevice(ctx->device));
+    TRY(ensure_work(ctx, c, false));
+    TRY(h2d(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
+    DevState s = base_state(ctx);
+    s.sw_b = 0;
+    TRY(upload_state(ctx, s));
+    TRY(phase_gram(ctx, false));
+    TRY(phase_combine(ctx, 1, 0));
+    TRY(phase_finalize(ctx, kFinGranular, 1));
+    TRY(d2h(ctx, g_out, ctx->d_gfull[0], (size_t)c * c * sizeof(double)));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return FC_OK;
+}
+
+static int pass_on_u0(fc_ctx* ctx, uint32_t c, double* merge_out) {
+    DevState s = base_state(ctx);
+    s.sw_b = 0;
+    TRY(upload_state(ctx, s));
+    TRY(phase_sweep(ctx, false));
+    TRY(phase_rowsum(ctx, 0));
+    TRY(phase_combine(ctx, 0, 1));
+    if (merge_out) {
+        const size_t slot = (ctx->shards.size() - 1) * nchains_of(c) + 2 * (size_t)npairs_of(c) + kScalMerge;
+        TRY(d2h(ctx, merge_out, ctx->d_totals + slot, sizeof(double)));
+    }
+    return FC_OK;
+}
+
+int fc_fused_column_pass(fc_ctx* ctx, uint32_t c, const double* x, double* xs_out, double* merge_out) {
+    if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
+    CU(cudaSetDevice(ctx->device));
+    TRY(ensure_work(ctx, c, false));
+    TRY(h2d(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
+    TRY(pass_on_u0(ctx, c, merge_out));
+    if (xs_out) TRY(d2h(ctx, xs_out, ctx->d_xs[0], ctx->n * c * sizeof(double)));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return FC_OK;
+}
+
+int fc_loss_decomposed(fc_ctx* ctx, uint32_t c, const double* x, const double* g, double* loss_out) {
+    double merge = 0.0;
+    TRY(fc_fused_column_pass(ctx, c, x, nullptr, &merge));
+    double fg = 0.0;   // ShareMatrix::frob_sq, objective.hpp:25-29
+    for (size_t k = 0; k < (size_t)c * c; ++k) fg += g[k] * g[k];
+    *loss_out = ctx->frob_s + fg - 2.0 * merge;
+    return FC_OK;
+}
+
+static int step_from_u0(fc_ctx* ctx, uint32_t c, const double* g, double tau, double* x_out) {
+    // k_step reads Gt[l*C + r] == G[r][l]
+    std::vector<double> gt((size_t)c * c);
+    for (uint32_t r = 0; r < c; ++r)
+        for (uint32_t l = 0; l < c; ++l) gt[(size_t)l * c + r] = g[(size_t)r * c + l];
+    TRY(h2d(ctx, ctx->d_gfull[0], gt.data(), gt.size() * sizeof(double)));
+    DevState s = base_state(ctx);
+    s.step_mode = kLiteral;
+    s.step_a = 0;
+    s.step_b = 0;
+    s.step_dst = 1;
+    s.step_sel = kMatExt;
+    s.xs_r = 0;
+    s.tau = tau;
+    TRY(upload_state(ctx, s));
+    TRY(phase_step(ctx, 0));
+    TRY(d2h(ctx, ctx->h_state, ctx->d_state, sizeof(DevState)));
+    TRY(d2h(ctx, x_out, ctx->d_U[1], ctx->n * c * sizeof(double)));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_state->error) return set_err(ctx, FC_INVALID, "project_simplex: non-finite entry");
+    return FC_OK;
+}
+
+int fc_gpa_step_fused(fc_ctx* ctx, uint32_t c, const double* x, const double* g, const double* xs, double tau,
+                      double* x_out) {
+    if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
+    CU(cudaSetDevice(ctx->device));
+    TRY(ensure_work(ctx, c, false));
+    TRY(h2d(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
+    TRY(h2d(ctx, ctx->d_xs[0], xs, ctx->n * c * sizeof(double)));
+    return step_from_u0(ctx, c, g, tau, x_out);
+}
+
+int fc_gpa_step(fc_ctx* ctx, uint32_t c, const double* x, const double* g, double tau, double* x_out) {
+    if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
+    CU(cudaSetDevice(ctx->device));
+    TRY(ensure_work(ctx, c, false));
+    TRY(h2d(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
+    TRY(pass_on_u0(ctx, c, nullptr));
+    return step_from_u0(ctx, c, g, tau, x_out);
+}
+
+int fc_project_simplex_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, double* x) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    if (c == 0) return set_err(ctx, FC_INVALID, "project_simplex: empty vector");
+    if (c > 256) return set_err(ctx, FC_INVALID, "cluster count C=%u exceeds the supported maximum 256", c);
+    if (rows == 0) return FC_OK;
+    CU(cudaSetDevice(ctx->device));
+    double* d = nullptr;
+    CU(cudaMallocAsync(&d, rows * c * sizeof(double), ctx->stream));
+    CU(cudaMemcpyAsync(d, x, rows * c * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemsetAsync(ctx->d_counter + 63, 0, sizeof(unsigned), ctx->stream));
+    int rc = by_c<LaunchProject>(ctx, c, ctx, d, (unsigned long long)rows, (int)c, ctx->d_counter + 63);
+    unsigned bad = 0;
+    if (!rc) {
+        CU(cudaMemcpyAsync(x, d, rows * c * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(&bad, ctx->d_counter + 63, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CU(cudaFreeAsync(d, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (rc) return rc;
+    if (bad) return set_err(ctx, FC_INVALID, "project_simplex: non-finite entry");
+    return FC_OK;
+}
+
+// ---- solver --------------------------------------------------------------------------
+int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const double* x0) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    CU(cudaSetDevice(ctx->device));
+    ctx->session = false;
+    // SolverConfig::validate, solver.hpp:40-47
+    if (cfg->max_iter < 1) return set_err(ctx, FC_INVALID, "solver: max_iter must be >= 1");
+    if (cfg->tol < 0.0) return set_err(ctx, FC_INVALID, "solver: tol must be >= 0");
+    if (cfg->trace_every < 1) return set_err(ctx, FC_INVALID, "solver: trace_every must be >= 1");
+    if (!(cfg->step_size > 0.0) && cfg->step_size != 0.0)
+        return set_err(ctx, FC_INVALID, "solver: step_size must be positive (or 0 for auto)");
+    if (cfg->method < FC_GPA || cfg->method > FC_FISTA_BT) return set_err(ctx, FC_INVALID, "solver: unknown method");
+    const bool bt = cfg->method == FC_FISTA_BT;
+    if (bt && !(cfg->bt_eta > 1.0)) return set_err(ctx, FC_INVALID, "solver: backtracking eta must be > 1");
+    if (bt && ctx->world > 1)
+        return set_err(ctx, FC_INVALID, "solver: backtracking FISTA needs a single-rank context");
+    if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
+    if (c == 0) return set_err(ctx, FC_INVALID, "membership: empty matrix");
+    TRY(ensure_work(ctx, c, bt));
+    TRY(ensure_trace(ctx, std::min<uint64_t>(cfg->max_iter + 2, 1u << 20)));
+
+    TRY(h2d(ctx, ctx->d_U[0], x0, ctx->n * c * sizeof(double)));
+    TRY(validate_x(ctx, 0, 1e-9));   // x0.validate(1e-9), solver.hpp:140 / :191
+
+    // resolve_step_size, solver.hpp:78-85
+    const double tau = cfg->step_size > 0.0 ? cfg->step_size
+                                            : 1.0 / (4.0 * std::sqrt(ctx->frob_s) + 12.0 * (double)ctx->n);
+    DevState s = base_state(ctx);
+    s.method = cfg->method;
+    s.max_iter = cfg->max_iter;
+    s.trace_every = cfg->trace_every;
+    s.tol = cfg->tol;
+    s.restart = cfg->fista_restart ? 1 : 0;
+    s.bt = bt ? 1 : 0;
+    s.bt_eta = cfg->bt_eta;
+    s.bt_max = (int)cfg->bt_max;
+    s.tau = tau;
+    s.tau0 = tau;
+    s.L = 1.0 / tau;
+    s.sw_b = 0;
+    s.sw_p = 0;
+    s.result_buf = 0;
+    s.reason = FC_MAX_ITER;
+    s.loss_prev = (double)ctx->n * (double)ctx->n;   // GPA: loss^{-1} := N^2 (solver.hpp:149-151)
+    s.xs_r = 0;
+    s.xs_w = 0;
+    TRY(upload_state(ctx, s));
+    k_stamp<<<1, 1, 0, ctx->stream>>>(ctx->d_state);   // device clock origin of elapsed_ms
+    TRY(check_launch(ctx, "k_stamp"));
+    ctx->method = cfg->method;
+    ctx->max_iter = cfg->max_iter;
+    ctx->enqueued = 0;
+    ctx->host_iter = cfg->method == FC_GPA ? 0 : 1;
+    ctx->session = true;
+    if (cfg->method != FC_GPA) TRY(enqueue_prelude(ctx));
+    return FC_OK;
+}
+
+int fc_solver_run(fc_ctx* ctx, uint64_t iterations) {
+    if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
+    CU(cudaSetDevice(ctx->device));
+    for (uint64_t k = 0; k < iterations; ++k) {
+        if (ctx->method == FC_GPA) TRY(enqueue_gpa_iteration(ctx));
+        else TRY(enqueue_fista_iteration(ctx, ctx->method == FC_FISTA_BT));
+        ctx->enqueued++;
+    }
+    return FC_OK;
+}
+
+static int session_done(fc_ctx* ctx, int* done) {
+    TRY(download_state(ctx));
+    prof_harvest(ctx);
+    if (ctx->h_state->error) {
+        ctx->session = false;
+        return set_err(ctx, FC_INVALID, "project_simplex: non-finite entry");
+    }
+    *done = ctx->h_state->done;
+    return FC_OK;
+}
+
+int fc_solver_sync(fc_ctx* ctx, int* done) {
+    if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
+    CU(cudaSetDevice(ctx->device));
+    return session_done(ctx, done);
+}
+
+int fc_solver_end(fc_ctx* ctx, double* x_out, fc_trace_record* trace, uint64_t trace_cap, fc_solve_summary* out) {
+    if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
+    CU(cudaSetDevice(ctx->device));
+    int done = 0;
+    TRY(session_done(ctx, &done));
+    const DevState& s = *ctx->h_state;
+    if (x_out) TRY(d2h(ctx, x_out, ctx->d_U[s.result_buf], ctx->n * ctx->c * sizeof(double)));
+    const uint64_t nrec = std::min<uint64_t>(std::min<uint64_t>(s.n_records, ctx->trace_alloc), trace_cap);
+    if (trace && nrec) TRY(d2h(ctx, trace, ctx->d_trace, nrec * sizeof(fc_trace_record)));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (out) {
+        out->reason = s.reason;
+        out->pad = 0;
+        out->iterations = s.iterations;
+        out->final_loss = s.final_loss;
+        out->step_size = s.tau0;
+        out->n_records = s.n_records;
+    }
+    ctx->session = false;
+    return FC_OK;
+}
+
+// Whole solve with a one-chunk-behind stop check (identical decisions on every
+// rank, so every rank enqueues the same collectives).
+int fc_solve(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const double* x0, double* x_out,
+             fc_trace_record* trace, uint64_t trace_cap, fc_solve_summary* out) {
+    TRY(fc_solver_begin(ctx, cfg, c, x0));
+    const bool bt = cfg->method == FC_FISTA_BT;
+    const uint64_t passes = cfg->method == FC_GPA ? cfg->max_iter + 1 : cfg->max_iter;
+    const uint64_t limit = bt ? passes * ((uint64_t)cfg->bt_max + 1) : passes;
+    const uint64_t chunk = 8;
+    uint64_t issued = 0, chunks = 0;
+    int pending = -1;
+    while (issued < limit) {
+        const uint64_t k = std::min(chunk, limit - issued);
+        TRY(fc_solver_run(ctx, k));
+        issued += k;
+        const int slot = (int)(chunks++ & 1);
+        CU(cudaMemcpyAsync(&ctx->h_done[slot], &ctx->d_state->done, sizeof(int), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaEventRecord(ctx->chunk_ev[slot], ctx->stream));
+        if (pending >= 0) {
+            CU(cudaEventSynchronize(ctx->chunk_ev[pending]));
+            if (ctx->h_done[pending]) break;
+        }
+        pending = slot;
+    }
+    return fc_solver_end(ctx, x_out, trace, trace_cap, out);
+}
+
+// ---- instrumentation -----------------------------------------------------------------
+void* fc_stream(fc_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+uint64_t fc_launch_count(const fc_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int fc_set_profiling(fc_ctx* ctx, int enabled) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    prof_harvest(ctx);
+    for (int k = 0; k < kNumCls; ++k) { ctx->prof_ms[k] = 0; ctx->prof_n[k] = 0; }
+    ctx->profiling = enabled != 0;
+    return FC_OK;
+}
+
+int fc_kernel_times(fc_ctx* ctx, double* ms, uint64_t* launches, int n_classes) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    prof_harvest(ctx);
+    for (int k = 0; k < n_classes && k < kNumCls; ++k) {
+        ms[k] = ctx->prof_ms[k];
+        launches[k] = ctx->prof_n[k];
+    }
+    return FC_OK;
+}
+
+int fc_generate_graph(const fc_graph_spec* spec, uint64_t* nnz_out, int64_t** row_ptr_out, uint32_t** col_idx_out) {
+    std::string err;
+    const int rc = fc_generate_graph_impl(spec, nnz_out, row_ptr_out, col_idx_out, &err);
+    if (rc) set_err(nullptr, rc, "%s", err.c_str());
+    return rc;
+}
+
+void fc_free(void* p) { std::free(p); }
+
+}  // extern "C"

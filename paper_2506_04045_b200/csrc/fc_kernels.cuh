@@ -1,0 +1,904 @@
+// fc_kernels.cuh -- sm_100a kernels of the GPA/FISTA hot path.
+//
+// Arithmetic contract: IEEE FP64, round-to-nearest, no FMA
+// contraction (the whole library is compiled with --fmad=false and the critical
+// expressions below use explicit __dmul_rn/__dadd_rn/__dsub_rn), every reduction
+// in the reference's fixed order.  The results are therefore bitwise identical to
+// the reference CPU solver (/root/reference/proj/include/fuzzyclust).
+//
+// Layout in HBM:
+//   U  : N x C f64 row-major (== the reference's C x N column-major X), node i's
+//        C memberships contiguous.  Three full replicas rotate (bar^n, bar^{n-1},
+//        bar^{n-2}) for FISTA, two for GPA.
+//   S  : CSR (== the reference's CSC, S symmetric) row_ptr i64, col u32, val f64
+//        (val absent when every value is 1.0: 1.0*x == x exactly).
+//   xs : shard rows x C f64 (S U products), two slots (0 = extrapolated point, 1 = bar).
+//   per-1024-row-block partials: Gram (packed upper triangle) and scalar terms.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fc {
+
+constexpr uint32_t kBlock = 1024;   // parallel.hpp:15 kReductionBlock
+constexpr unsigned kFull = 0xffffffffu;
+
+enum : int { kLiteral = 0, kExtrap = 1 };
+enum : int { kMatExt = 0, kMatBar = 1 };
+// scalar partial / total slots
+enum : int { kScalMerge = 0, kScalLin = 1, kScalSq = 2, kScalMergeY = 3, kNumScal = 4 };
+enum : int { kFinPrelude = 0, kFinFista = 1, kFinGpa = 2, kFinGranular = 3 };
+
+// Solver state in device memory.  Kernels read the "plan" fields; only
+// k_finalize (one thread) writes them, so a whole iteration can be enqueued
+// (or graph-replayed) without host round trips.
+struct DevState {
+    unsigned long long iter;        // iteration whose pass is being computed
+    unsigned long long n_records;
+    unsigned long long iterations;  // SolverTrace::iterations
+    unsigned long long max_iter;
+    unsigned long long trace_every;
+    unsigned long long trace_cap;
+    int done;
+    int error;                      // 1: non-finite projection input
+    int reason;
+    int method;
+    int restart;                    // fista_restart
+    int bt;                         // backtracking enabled
+    int bt_max;
+    int backtracks;                 // backtracks taken in the current iteration
+    double loss_prev;
+    double final_loss;
+    double t;                       // FISTA t_n
+    double tau;                     // step used by the next k_step
+    double tau0;
+    double L;                       // backtracking: 1/tau
+    double bt_eta;
+    double frob_s;                  // ||S||_F^2
+    double tol;
+    double frob_gy;                 // backtracking: ||G(y)||^2 of the current y
+    // plan of the next k_step
+    int step_mode;                  // kLiteral | kExtrap
+    int step_a;                     // U index of bar^{n-1} (or literal source)
+    int step_b;                     // U index of bar^{n-2}
+    int step_dst;                   // U index receiving bar^n
+    int step_sel;                   // 0: use (G, xs) of the extrapolated point, 1: of bar
+    int sw_b;                       // U index of the point swept / Gram'd (bar^n)
+    int sw_p;                       // U index of bar^{n-1} (dual pass)
+    int result_buf;                 // U index holding result.membership
+    double beta_step;               // beta used to rebuild X_ext^n in k_step
+    double beta_next;               // beta_n: X_ext^{n+1} = bar^n + beta_n (bar^n - bar^{n-1})
+    long long t0_ns;
+    int xs_r;                       // xs set read by k_step (S y of the current y)
+    int xs_w;                       // xs set written by k_sweep (differs only with backtracking)
+    unsigned long long err_bits;    // validation: max feasibility error (as bits)
+    unsigned int nonfinite;
+    unsigned int pad;
+};
+
+struct TraceRec {                   // == fc_trace_record
+    unsigned long long iteration;
+    double loss;
+    double elapsed_ms;
+    int loss_increased;
+    int backtracks;
+    double step;
+};
+
+// Everything a kernel needs, passed by value.  Row-indexed shard arrays (xs,
+// prod, rowterm) and block-indexed partials are pre-offset to the shard.
+struct Bufs {
+    const long long* row_ptr;       // shard-local, rebased (row_ptr[0] == 0)
+    const unsigned* col;
+    const double* val;              // nullptr => pattern only
+    double* U[3];
+    double* xs[4];                  // [set*2 + slot]; set = DevState::xs_r / xs_w
+    double* prod;                   // per row: <xs_bar_i, bar_i> (or <xs_i, x_i>)
+    double* rowterm[3];             // backtracking: lin_i, sq_i, <xs_y_i, y_i>
+    double* gpart[2];               // [blk][npairs]
+    double* spart;                  // [scal][spart_stride]
+    double* totals;                 // [2*npairs + kNumScal]
+    double* gfull[2];               // C x C, read as Gt[l*C + r] == G[r][l]
+    TraceRec* trace;
+    DevState* st;
+    unsigned* counter;              // dynamic row scheduler of k_sweep
+};
+
+struct Geo {
+    unsigned C;
+    unsigned npairs;
+    unsigned long long N;
+    unsigned long long row0;        // first global row of the shard (multiple of 1024)
+    unsigned long long nrows;
+    unsigned long long nblk;        // blocks of the shard
+    unsigned long long spart_stride;
+};
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+// std::max(a, b) as the reference uses it: (a < b) ? b : a
+__device__ __forceinline__ double ref_max(double a, double b) { return (a < b) ? b : a; }
+// FISTA extrapolation, solver.hpp:261: b + beta * (b - p)
+__device__ __forceinline__ double extrap(double b, double p, double beta) {
+    return dadd(b, dmul(beta, dsub(b, p)));
+}
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+__host__ __device__ __forceinline__ unsigned pair_index(unsigned r, unsigned s, unsigned C) {
+    // packed upper triangle, r <= s, row-major
+    return r * C - (r * (r - 1u)) / 2u + (s - r);
+}
+
+// =============================================================================
+// Per-row simplex projection, lane-parallel within a group of G lanes
+// (component r lives in lane r % G, slot r / G).  Follows simplex.hpp:18-59
+// operation for operation:
+//   sort descending; cumsum; t_k = (cs_k - 1)/(k+1); last k with s_k - t_k >= 0;
+//   y = max(y - thr, 0); up to 4 residual folds onto the (tied) maxima.
+// sm: G*S doubles of group-private shared scratch.
+// Returns false if any entry was non-finite (the reference throws InvalidInput).
+// =============================================================================
+template <int G, int S>
+__device__ __forceinline__ bool project_group(double (&y)[S], int C, int lg, double* sm) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned gbase = lane & ~(unsigned)(G - 1);
+    const unsigned gbits = (G == 32) ? kFull : (((1u << G) - 1u) << gbase);
+
+    __syncwarp();   // sm is reused row after row: finish the previous row's reads
+    bool fin = true;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int r = lg + s * G;
+        if (r < C && !isfinite(y[s])) fin = false;
+    }
+    const bool all_fin = (__ballot_sync(kFull, !fin) & gbits) == 0u;
+    if (C == 1) {   // uniform across the warp
+        if (lg == 0) y[0] = 1.0;
+        return all_fin;
+    }
+    if (!all_fin) {
+        // the reference throws; keep this group's lanes convergent with the rest
+        // of the warp on harmless values (the caller raises the error flag)
+#pragma unroll
+        for (int s = 0; s < S; ++s) y[s] = 0.0;
+    }
+
+    // rank of each of my components in the descending order (ties by index)
+    int rank[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) rank[s] = 0;
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) {
+#pragma unroll
+        for (int l2 = 0; l2 < G; ++l2) {
+            const int l = s2 * G + l2;
+            const double v = __shfl_sync(kFull, y[s2], l2, G);
+            if (l < C) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int r = lg + s * G;
+                    rank[s] += (v > y[s]) || (v == y[s] && l < r);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int r = lg + s * G;
+        if (r < C) sm[rank[s]] = y[s];
+    }
+    __syncwarp();
+
+    // cumsum in sorted order (sequential, as the reference) -- each lane-slot
+    // keeps the partial sum at the sorted position it owns (k = lg + s*G)
+    double mycs[S];
+    double cs = 0.0;
+    for (int k = 0; k < C; ++k) {
+        cs = dadd(cs, sm[k]);
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (k == lg + s * G) mycs[s] = cs;
+    }
+    double tk[S];
+    int best = -1;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int k = lg + s * G;
+        bool cond = false;
+        tk[s] = 0.0;
+        if (k < C) {
+            tk[s] = dsub(mycs[s], 1.0) / (double)(k + 1);
+            cond = dsub(sm[k], tk[s]) >= 0.0;
+        }
+        const unsigned bal = (__ballot_sync(kFull, cond) & gbits) >> gbase;
+        if (bal) best = max(best, s * G + (31 - __clz(bal)));
+    }
+    double thr = 0.0;
+    if (best >= 0) {
+        const int bl = best % G, bs = best / G;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const double v = __shfl_sync(kFull, tk[s], bl, G);
+            if (s == bs) thr = v;
+        }
+    } else {
+        // keep the shuffles warp-convergent for other groups of the warp
+#pragma unroll
+        for (int s = 0; s < S; ++s) (void)__shfl_sync(kFull, tk[s], 0, G);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int r = lg + s * G;
+        if (r < C) y[s] = ref_max(dsub(y[s], thr), 0.0);
+    }
+
+    // residual folds (simplex.hpp:43-55)
+    bool live = true;
+    for (int round = 0; round < 4; ++round) {
+        double sum = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) {
+#pragma unroll
+            for (int l2 = 0; l2 < G; ++l2) {
+                const double v = __shfl_sync(kFull, y[s2], l2, G);
+                if (s2 * G + l2 < C) sum = dadd(sum, v);
+            }
+        }
+        const double residual = dsub(sum, 1.0);
+        if (residual == 0.0) live = false;
+        double top = -INFINITY;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (lg + s * G < C) top = (top < y[s]) ? y[s] : top;
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            const double v = __shfl_xor_sync(kFull, top, o, G);
+            top = (top < v) ? v : top;
+        }
+        int ties = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const bool eq = (lg + s * G < C) && (y[s] == top);
+            ties += __popc(__ballot_sync(kFull, eq) & gbits);
+        }
+        if (!__any_sync(kFull, live)) break;
+        if (live) {
+            const double share = residual / (double)ties;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                if (lg + s * G < C && y[s] == top) y[s] = ref_max(dsub(y[s], share), 0.0);
+        }
+    }
+    return all_fin;
+}
+
+// Sequential (index-order) sum over a group's components of a[]:
+//   p = 0; p += a_0; p += a_1; ...  (loss_terms_column, objective.hpp:131-135)
+template <int G, int S>
+__device__ __forceinline__ double group_seq_sum(const double (&a)[S], int C) {
+    double p = 0.0;
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) {
+#pragma unroll
+        for (int l2 = 0; l2 < G; ++l2) {
+            const double v = __shfl_sync(kFull, a[s2], l2, G);
+            if (s2 * G + l2 < C) p = dadd(p, v);
+        }
+    }
+    return p;
+}
+
+// =============================================================================
+// K1: CSR SpMM sweep with the loss-term epilogue.
+//   xs_i[r] = sum_{k in row i, ascending} w_k * X[j_k][r]      (objective.hpp:98-109)
+//   prod_i  = sum_r xs_i[r] * x_i[r]                            (objective.hpp:131-135)
+// DUAL (the FISTA single-sweep schedule): one pass over
+// the CSR gathers bar^n_j and bar^{n-1}_j and accumulates both
+//   S bar^n                and   S X_ext^{n+1},  X_ext^{n+1}_j = bar_j + beta (bar_j - prev_j)
+// where each X_ext entry is formed exactly as solver.hpp:261 forms it, so both
+// sums are bit-identical to the reference's two separate sweeps.
+// Work: groups of G lanes own a row; warps pull 32-row chunks from a counter.
+// =============================================================================
+template <int G, int S, bool DUAL, bool W>
+__global__ void __launch_bounds__(256) k_sweep(Bufs b, Geo g) {
+    const DevState* st = b.st;
+    if (st->done) return;
+    constexpr int U = (G < 8) ? G : 8;
+    constexpr int RPW = 32 / G;           // rows per warp pass
+    constexpr unsigned kChunk = 32;       // rows per scheduler grab
+    const int C = (int)g.C;
+    const double* __restrict__ B = b.U[st->sw_b];
+    const double* __restrict__ P = DUAL ? b.U[st->sw_p] : nullptr;
+    const double beta = st->beta_next;
+    const unsigned lane = threadIdx.x & 31u;
+    const int lg = (int)(lane % G);
+    const int sub = (int)(lane / G);
+    double* xs_main = DUAL ? b.xs[st->xs_w * 2 + kMatBar] : b.xs[st->xs_w * 2 + kMatExt];
+    double* xs_ext = b.xs[st->xs_w * 2 + kMatExt];
+
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(b.counter, kChunk);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= g.nrows) break;
+        for (unsigned off = 0; off < kChunk; off += RPW) {
+            const unsigned long long row = base + off + sub;
+            const bool active = row < g.nrows;
+            if (!__any_sync(kFull, active)) break;
+            long long e0 = 0, e1 = 0;
+            if (active) {
+                e0 = b.row_ptr[row];
+                e1 = b.row_ptr[row + 1];
+            }
+            double ab[S], ae[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) { ab[s] = 0.0; ae[s] = 0.0; }
+
+            for (long long eb = e0;; eb += G) {
+                const bool more = eb < e1;
+                if (!__any_sync(kFull, more)) break;
+                unsigned myj = 0;
+                double myw = 1.0;
+                if (eb + lg < e1) {
+                    myj = __ldg(b.col + eb + lg);
+                    if (W) myw = ldg(b.val + eb + lg);
+                }
+                const int cnt = more ? (int)min((long long)G, e1 - eb) : 0;
+#pragma unroll
+                for (int k0 = 0; k0 < G; k0 += U) {
+                    double vb[U][S];
+                    double vp[DUAL ? U : 1][S];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const unsigned j = __shfl_sync(kFull, myj, k0 + u, G);
+                        const bool ok = (k0 + u) < cnt;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            const int r = lg + s * G;
+                            const bool okc = ok && r < C;
+                            const size_t a = (size_t)j * (size_t)C + (size_t)r;
+                            vb[u][s] = okc ? ldg(B + a) : 0.0;
+                            if (DUAL) vp[u][s] = okc ? ldg(P + a) : 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const double w = W ? __shfl_sync(kFull, myw, k0 + u, G) : 1.0;
+                        if ((k0 + u) < cnt) {
+#pragma unroll
+                            for (int s = 0; s < S; ++s) {
+                                ab[s] = W ? dadd(ab[s], dmul(w, vb[u][s])) : dadd(ab[s], vb[u][s]);
+                                if (DUAL) {
+                                    const double e = extrap(vb[u][s], vp[u][s], beta);
+                                    ae[s] = W ? dadd(ae[s], dmul(w, e)) : dadd(ae[s], e);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            // epilogue: store xs rows, prod_i
+            double a[S];
+            const unsigned long long grow = g.row0 + row;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int r = lg + s * G;
+                a[s] = 0.0;
+                if (active && r < C) {
+                    const double xi = ldg(B + (size_t)grow * C + r);
+                    a[s] = dmul(ab[s], xi);
+                    xs_main[(size_t)row * C + r] = ab[s];
+                    if (DUAL) xs_ext[(size_t)row * C + r] = ae[s];
+                }
+            }
+            const double p = group_seq_sum<G, S>(a, C);
+            if (active && lg == 0) b.prod[row] = p;
+        }
+    }
+}
+
+// =============================================================================
+// Per-block sequential sums of per-row scalars (objective.hpp:160-170 order):
+//   part[s][blk] = ((0 + v_{1024 blk}) + v_{1024 blk + 1}) + ...
+// One thread per (scalar, block).
+// =============================================================================
+__global__ void __launch_bounds__(128) k_rowsum(Bufs b, Geo g, int nscal, const double* a0,
+                                                const double* a1, const double* a2, const double* a3,
+                                                int slot0) {
+    if (b.st->done) return;
+    const unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (t >= g.nblk * (unsigned long long)nscal) return;
+    const int which = (int)(t / g.nblk);
+    const unsigned long long blk = t % g.nblk;
+    const double* a = which == 0 ? a0 : which == 1 ? a1 : which == 2 ? a2 : a3;
+    const unsigned long long r0 = blk * kBlock;
+    const unsigned long long r1 = min(r0 + kBlock, g.nrows);
+    double m = 0.0;
+    unsigned long long i = r0;
+    for (; i + 8 <= r1; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = a[i + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m = dadd(m, v[u]);
+    }
+    for (; i < r1; ++i) m = dadd(m, a[i]);
+    b.spart[(size_t)(slot0 + which) * g.spart_stride + blk] = m;
+}
+
+// =============================================================================
+// K2: Gram partials per 1024-row block, objective.hpp:69-80:
+//   P_b[r][s] = sum_{i in block b, ascending} x_i[r] * x_i[s]
+// x_i[r]*x_i[s] == x_i[s]*x_i[r] in IEEE, so only r <= s is accumulated (the
+// reference's matrix is exactly symmetric).  Each thread owns a 4x4 register
+// tile of (r, s) of one matrix and walks the block's rows in order from
+// shared-memory chunks.  dual: matrix 1 = bar^n, matrix 0 = X_ext^{n+1}
+// (formed as in solver.hpp:261); single: matrix 0 = the swept point.
+// grid = (blocks, tile groups); blockDim = 128.
+// =============================================================================
+constexpr int kGramThreads = 128;
+
+__global__ void __launch_bounds__(kGramThreads) k_gram(Bufs b, Geo g, int dual, int rows_per_chunk) {
+    const DevState* st = b.st;
+    if (st->done) return;
+    extern __shared__ double smg[];
+    const int C = (int)g.C;
+    const int C4 = (C + 3) & ~3;
+    const int nT = C4 / 4;
+    const int tiles_per_mat = nT * (nT + 1) / 2;
+    const int nmat = dual ? 2 : 1;
+    const int tile = blockIdx.y * kGramThreads + threadIdx.x;
+    const bool has = tile < tiles_per_mat * nmat;
+    const int mat_local = has ? tile / tiles_per_mat : 0;
+    int tt = has ? tile % tiles_per_mat : 0;
+    int I = 0;
+    while (tt >= nT - I) { tt -= nT - I; ++I; }
+    const int J = I + tt;
+    // dual: local matrix 0 -> bar (slot kMatBar), 1 -> ext (slot kMatExt)
+    const int out_mat = dual ? (mat_local == 0 ? kMatBar : kMatExt) : kMatExt;
+
+    const double* __restrict__ Bm = b.U[st->sw_b];
+    const double* __restrict__ Pm = dual ? b.U[st->sw_p] : nullptr;
+    const double beta = st->beta_next;
+    const unsigned long long blk = blockIdx.x;
+    const unsigned long long r0 = blk * kBlock;
+    const unsigned long long r1 = min(r0 + kBlock, g.nrows);
+    const int R = rows_per_chunk;
+    double* tb = smg;                       // [R][C4] bar / single
+    double* te = smg + (size_t)R * C4;      // [R][C4] ext
+
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+
+    for (unsigned long long cr = r0; cr < r1; cr += R) {
+        const int rows = (int)min((unsigned long long)R, r1 - cr);
+        __syncthreads();
+        for (int e = threadIdx.x; e < rows * C4; e += kGramThreads) {
+            const int rr = e / C4, cc = e % C4;
+            double vb = 0.0, ve = 0.0;
+            if (cc < C) {
+                const size_t a = (size_t)(g.row0 + cr + rr) * C + cc;
+                vb = Bm[a];
+                if (dual) ve = extrap(vb, Pm[a], beta);
+            }
+            tb[rr * C4 + cc] = vb;
+            if (dual) te[rr * C4 + cc] = ve;
+        }
+        __syncthreads();
+        if (has) {
+            const double* t = mat_local == 0 ? tb : te;
+            for (int rr = 0; rr < rows; ++rr) {
+                const double* rowp = t + rr * C4;
+                double xr[4], xq[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) { xr[a] = rowp[4 * I + a]; xq[a] = rowp[4 * J + a]; }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[a][c] = dadd(acc[a][c], dmul(xr[a], xq[c]));
+            }
+        }
+    }
+    if (has) {
+        double* out = b.gpart[out_mat] + (size_t)blk * g.npairs;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int r = 4 * I + a, s = 4 * J + c;
+                if (r <= s && s < C) out[pair_index(r, s, C)] = acc[a][c];
+            }
+    }
+}
+
+// =============================================================================
+// K4a: ordered combine of block partials (objective.hpp:82-88, :171):
+//   total = ((init + part_0) + part_1) + ...   one thread per chain.
+// Chains: [mat 0 pairs][mat 1 pairs][scalars].  `init` carries the running
+// total of the previous shard (multi-GPU ordered chain) or is null (0.0).
+// =============================================================================
+__global__ void __launch_bounds__(128) k_combine(Bufs b, Geo g, int mat_mask, int scal_mask,
+                                                 const double* init) {
+    if (b.st->done) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int np = (int)g.npairs;
+    const double* src;
+    size_t stride;
+    if (t < 2 * np) {
+        const int m = t / np;
+        if (!((mat_mask >> m) & 1)) return;
+        src = b.gpart[m] + (t % np);
+        stride = np;
+    } else {
+        const int s = t - 2 * np;
+        if (s >= kNumScal || !((scal_mask >> s) & 1)) return;
+        src = b.spart + (size_t)s * g.spart_stride;
+        stride = 1;
+    }
+    double acc = init ? init[t] : 0.0;
+    unsigned long long k = 0;
+    for (; k + 8 <= g.nblk; k += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = src[(k + u) * stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = dadd(acc, v[u]);
+    }
+    for (; k < g.nblk; ++k) acc = dadd(acc, src[k * stride]);
+    b.totals[t] = acc;
+}
+
+__device__ __forceinline__ double packed_at(const double* tot, int r, int s, int C) {
+    return r <= s ? tot[pair_index(r, s, C)] : tot[pair_index(s, r, C)];
+}
+
+// ||G||_F^2, sequential over the row-major entries (objective.hpp:25-29)
+__device__ double frob_packed(const double* tot, int C) {
+    double f = 0.0;
+    for (int r = 0; r < C; ++r)
+        for (int s = 0; s < C; ++s) {
+            const double v = packed_at(tot, r, s, C);
+            f = dadd(f, dmul(v, v));
+        }
+    return f;
+}
+
+__device__ double fista_t_next(double t) {     // solver.hpp:72
+    return (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+}
+
+__device__ __forceinline__ void push_record(Bufs& b, DevState* st, unsigned long long it, double loss,
+                                            int increased, int backtracks, double step) {
+    const unsigned long long k = st->n_records++;
+    if (k < st->trace_cap) {
+        long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        TraceRec& r = b.trace[k];
+        r.iteration = it;
+        r.loss = loss;
+        r.elapsed_ms = (double)(now - st->t0_ns) * 1e-6;
+        r.loss_increased = increased;
+        r.backtracks = backtracks;
+        r.step = step;
+    }
+}
+
+// =============================================================================
+// K4b: loss, stop rule, trace record and next-iteration plan (one CTA).
+//   loss = (||S||^2 + ||G||^2) - 2 merge          solver.hpp:156 / :224
+//   GPA stop:   loss_prev - loss <= tol           solver.hpp:157-173
+//   FISTA stop: (loss_prev - loss <= tol) && !(increased && restart), restart
+//               and momentum update               solver.hpp:224-269
+// Expands the combined Gram(s) to full C x C (gfull) for the next k_step.
+// =============================================================================
+// Decision part of k_finalize (thread 0).  Returns whether the combined Gram
+// matrices become the next step's (false only on a rejected backtracking trial,
+// which must keep G(y) and S y of the current extrapolated point).
+__device__ bool finalize_decide(Bufs& b, Geo& g, int kind) {
+    DevState* st = b.st;
+    const int C = (int)g.C;
+    const int np = (int)g.npairs;
+    const double* scal = b.totals + 2 * (size_t)np;
+    if (kind == kFinGranular) return true;
+
+    const int gm = (kind == kFinFista) ? kMatBar : kMatExt;
+    const double frob_g = frob_packed(b.totals + (size_t)gm * np, C);
+    const double loss = dsub(dadd(st->frob_s, frob_g), dmul(2.0, scal[kScalMerge]));
+    const unsigned long long n = st->iter;
+
+    if (kind == kFinPrelude) {                    // solver.hpp:206-215
+        st->loss_prev = loss;
+        st->final_loss = loss;
+        st->iterations = 0;
+        st->reason = 1;                           // kMaxIter unless a stop rule fires
+        push_record(b, st, 0, loss, 0, 0, st->tau);
+        st->t = 1.0;
+        st->step_mode = kLiteral;
+        st->step_a = st->sw_b;
+        st->step_sel = kMatExt;
+        st->step_dst = (st->sw_b + 1) % 3;
+        st->beta_step = 0.0;
+        st->beta_next = (st->t - 1.0) / fista_t_next(st->t);
+        st->sw_p = st->sw_b;
+        st->sw_b = st->step_dst;
+        st->result_buf = st->sw_p;
+        if (st->bt) st->frob_gy = frob_g;
+        st->xs_r = st->xs_w;                      // S x0 is the first step's S y
+        if (st->bt) st->xs_w = 1 - st->xs_w;
+        st->iter = 1;
+        return true;
+    }
+
+    if (kind == kFinGpa) {                        // solver.hpp:153-178
+        const int increased = n > 0 && loss > st->loss_prev;
+        const bool stop_tol = dsub(st->loss_prev, loss) <= st->tol;
+        const bool stop_iter = n >= st->max_iter;
+        if (stop_tol || stop_iter || n % st->trace_every == 0)
+            push_record(b, st, n, loss, increased, 0, st->tau);
+        st->iterations = n;
+        st->final_loss = loss;
+        st->result_buf = st->sw_b;
+        if (stop_tol || stop_iter) {
+            st->reason = stop_tol ? 0 : 1;
+            st->done = 1;
+            return true;
+        }
+        st->step_mode = kLiteral;
+        st->step_a = st->sw_b;
+        st->step_sel = kMatExt;
+        st->step_dst = 1 - st->sw_b;
+        st->sw_b = st->step_dst;
+        st->loss_prev = loss;
+        st->iter = n + 1;
+        return true;
+    }
+
+    // kFinFista
+    if (st->bt) {                                 // Beck-Teboulle sufficient decrease
+        const double f_y = dsub(dadd(st->frob_s, st->frob_gy), dmul(2.0, scal[kScalMergeY]));
+        const double q = dadd(dadd(f_y, scal[kScalLin]), dmul(dmul(0.5, st->L), scal[kScalSq]));
+        if (loss > q && st->backtracks < st->bt_max) {
+            st->L = dmul(st->bt_eta, st->L);
+            st->tau = 1.0 / st->L;
+            st->backtracks += 1;
+            return false;                         // same iteration, same y, new step: keep G(y)
+        }
+    }
+    const int increased = loss > st->loss_prev;
+    const double decrease = dsub(st->loss_prev, loss);
+    const bool stop_tol = decrease <= st->tol && !(increased && st->restart);
+    const bool stop_iter = n >= st->max_iter;
+    if (stop_tol || stop_iter || n % st->trace_every == 0)
+        push_record(b, st, n, loss, increased, st->backtracks, st->tau);
+    st->result_buf = st->sw_b;
+    st->iterations = n;
+    st->final_loss = loss;
+    st->backtracks = 0;
+    if (stop_tol) {
+        st->reason = increased ? 2 : 0;
+        st->done = 1;
+        return true;
+    }
+    if (stop_iter) {
+        st->reason = 1;
+        st->done = 1;
+        return true;
+    }
+    const int bar_idx = st->sw_b, prev_idx = st->sw_p;
+    st->xs_r = st->xs_w;                          // this pass's S bar / S X_ext feed the next step
+    if (st->bt) st->xs_w = 1 - st->xs_w;
+    if (increased && st->restart) {               // solver.hpp:247-249
+        st->t = 1.0;
+        st->step_mode = kLiteral;
+        st->step_a = bar_idx;
+        st->step_sel = kMatBar;
+        if (st->bt) st->frob_gy = frob_g;
+    } else {                                      // solver.hpp:251-266
+        const double t_next = fista_t_next(st->t);
+        st->step_mode = kExtrap;
+        st->step_a = bar_idx;
+        st->step_b = prev_idx;
+        st->beta_step = st->beta_next;            // == (t - 1) / t_next
+        st->step_sel = kMatExt;
+        st->t = t_next;
+        if (st->bt) st->frob_gy = frob_packed(b.totals + (size_t)kMatExt * np, C);
+    }
+    st->beta_next = (st->t - 1.0) / fista_t_next(st->t);
+    st->step_dst = 3 - bar_idx - prev_idx;
+    st->sw_p = bar_idx;
+    st->sw_b = st->step_dst;
+    st->loss_prev = loss;
+    st->iter = n + 1;
+    return true;
+}
+
+__global__ void __launch_bounds__(256) k_finalize(Bufs b, Geo g, int kind, int mat_mask) {
+    DevState* st = b.st;
+    if (st->done) return;
+    __shared__ int expand;
+    const int C = (int)g.C;
+    const int np = (int)g.npairs;
+    if (threadIdx.x == 0) expand = finalize_decide(b, g, kind) ? 1 : 0;
+    __syncthreads();
+    if (!expand) return;
+    for (int m = 0; m < 2; ++m) {
+        if (!((mat_mask >> m) & 1)) continue;
+        const double* tot = b.totals + (size_t)m * np;
+        for (int e = threadIdx.x; e < C * C; e += blockDim.x) {
+            const int r = e / C, s = e % C;
+            b.gfull[m][e] = packed_at(tot, r, s, C);
+        }
+    }
+}
+
+// =============================================================================
+// K3: gradient step + simplex projection (solver.hpp:89-107), with the FISTA
+// extrapolated point rebuilt on the fly (solver.hpp:261) instead of stored:
+//   x   = literal ? A_i : A_i + beta (A_i - B_i)
+//   o_r = sum_l G[r][l] x_l                    (ShareMatrix::apply, objective.hpp:37-43)
+//   g_r = -4 (xs_r - o_r)                      (objective.hpp:116-117)
+//   y_r = x_r - tau g_r ; bar = P_simplex(y)
+// bt: also lin_i = sum_r g_r (bar_r - x_r), sq_i = sum_r (bar_r - x_r)^2,
+//     <xs_i, x_i> (merge term of f at the extrapolated point).
+// =============================================================================
+template <int G, int S>
+__global__ void __launch_bounds__(256) k_step(Bufs b, Geo g, int bt) {
+    DevState* st = b.st;
+    if (st->done) return;
+    __shared__ double smp[256 / 32][32 / G][G * S];
+    const int C = (int)g.C;
+    const unsigned lane = threadIdx.x & 31u;
+    const int lg = (int)(lane % G);
+    const int sub = (int)(lane / G);
+    double* sm = &smp[threadIdx.x >> 5][sub][0];
+    const int mode = st->step_mode;
+    const double* __restrict__ A = b.U[st->step_a];
+    const double* __restrict__ Bp = b.U[st->step_b];
+    double* __restrict__ D = b.U[st->step_dst];
+    const double beta = st->beta_step;
+    const double tau = st->tau;
+    const int sel = st->step_sel;
+    const double* __restrict__ Gt = b.gfull[sel];
+    const double* __restrict__ XS = b.xs[st->xs_r * 2 + sel];
+
+    const unsigned long long warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    constexpr int RPW = 32 / G;
+    bool bad = false;
+    for (unsigned long long rb = w0 * RPW; rb < g.nrows; rb += warps * RPW) {
+        const unsigned long long row = rb + sub;
+        const bool active = row < g.nrows;
+        const unsigned long long grow = g.row0 + row;
+        double x[S], xs[S], y[S], gr[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int r = lg + s * G;
+            x[s] = 0.0;
+            xs[s] = 0.0;
+            if (active && r < C) {
+                const size_t a = (size_t)grow * C + r;
+                const double av = A[a];
+                x[s] = (mode == kLiteral) ? av : extrap(av, Bp[a], beta);
+                xs[s] = XS[(size_t)row * C + r];
+            }
+        }
+        double o[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) o[s] = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) {
+#pragma unroll
+            for (int l2 = 0; l2 < G; ++l2) {
+                const int l = s2 * G + l2;
+                const double xl = __shfl_sync(kFull, x[s2], l2, G);
+                if (l < C) {
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const int r = lg + s * G;
+                        if (r < C) o[s] = dadd(o[s], dmul(ldg(Gt + (size_t)l * C + r), xl));
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            gr[s] = dmul(-4.0, dsub(xs[s], o[s]));
+            y[s] = dsub(x[s], dmul(tau, gr[s]));
+        }
+        const bool ok = project_group<G, S>(y, C, lg, sm);
+        if (!ok && active) bad = true;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int r = lg + s * G;
+            if (active && r < C) D[(size_t)grow * C + r] = y[s];
+        }
+        if (bt) {
+            double al[S], aq[S], am[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const double d = dsub(y[s], x[s]);
+                al[s] = dmul(gr[s], d);
+                aq[s] = dmul(d, d);
+                am[s] = dmul(xs[s], x[s]);
+            }
+            const double li = group_seq_sum<G, S>(al, C);
+            const double qi = group_seq_sum<G, S>(aq, C);
+            const double mi = group_seq_sum<G, S>(am, C);
+            if (active && lg == 0) {
+                b.rowterm[0][row] = li;
+                b.rowterm[1][row] = qi;
+                b.rowterm[2][row] = mi;
+            }
+        }
+    }
+    if (bad) {
+        st->error = 1;
+        st->done = 1;
+    }
+}
+
+// Device clock origin of TraceRecord::elapsed_ms.
+__global__ void k_stamp(DevState* st) {
+    long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    st->t0_ns = now;
+}
+
+// Batched in-place projection (init_membership's per-column projection).
+template <int G, int S>
+__global__ void __launch_bounds__(256) k_project(double* x, unsigned long long rows, int C,
+                                                 unsigned* bad_flag) {
+    __shared__ double smp[256 / 32][32 / G][G * S];
+    const unsigned lane = threadIdx.x & 31u;
+    const int lg = (int)(lane % G);
+    const int sub = (int)(lane / G);
+    double* sm = &smp[threadIdx.x >> 5][sub][0];
+    const unsigned long long warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    constexpr int RPW = 32 / G;
+    for (unsigned long long rb = w0 * RPW; rb < rows; rb += warps * RPW) {
+        const unsigned long long row = rb + sub;
+        const bool active = row < rows;
+        double y[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int r = lg + s * G;
+            y[s] = (active && r < C) ? x[row * C + r] : 0.0;
+        }
+        const bool ok = project_group<G, S>(y, C, lg, sm);
+        if (!ok && active) atomicOr(bad_flag, 1u);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int r = lg + s * G;
+            if (active && r < C) x[row * C + r] = y[s];
+        }
+    }
+}
+
+// x0.validate(1e-9) (membership.hpp:49-61): non-finite flag + max feasibility
+// error (max is order independent; the per-column sum is sequential).
+__global__ void __launch_bounds__(256) k_validate(const double* x, unsigned long long n, int C, DevState* st) {
+    const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double sum = 0.0, worst = 0.0;
+    bool fin = true;
+    for (int k = 0; k < C; ++k) {
+        const double v = x[i * C + k];
+        if (!isfinite(v)) fin = false;
+        sum = dadd(sum, v);
+        if (v < 0.0) worst = worst < -v ? -v : worst;
+        if (v > 1.0) worst = worst < dsub(v, 1.0) ? dsub(v, 1.0) : worst;
+    }
+    const double dev = fabs(dsub(sum, 1.0));
+    worst = worst < dev ? dev : worst;
+    if (!fin) atomicOr(&st->nonfinite, 1u);
+    else if (worst > 0.0) atomicMax(&st->err_bits, (unsigned long long)__double_as_longlong(worst));
+}
+
+}  // namespace fc
