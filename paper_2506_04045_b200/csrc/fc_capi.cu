@@ -215,35 +215,62 @@ int grid_for(const void* fn, int threads, size_t smem, int sm_count) {
     return occ * sm_count;
 }
 
+template <int G, int S, bool DUAL, bool W, bool EXACT>
+int launch_sweep_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static int grid = 0;
+    if (!grid) grid = grid_for((const void*)k_sweep<G, S, DUAL, W, EXACT>, 256, 0, ctx->sm_count);
+    const unsigned long long need = (g.nrows + 31) / 32;   // 32-row chunks, 8 warps per CTA
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, (need + 7) / 8));
+    k_sweep<G, S, DUAL, W, EXACT><<<gr, 256, 0, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_sweep launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
 template <int G, int S>
 struct LaunchSweep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, bool dual) {
         if (g.nrows == 0) return FC_OK;
-        const void* fn;
-        if (dual) fn = ctx->weighted ? (const void*)k_sweep<G, S, true, true> : (const void*)k_sweep<G, S, true, false>;
-        else fn = ctx->weighted ? (const void*)k_sweep<G, S, false, true> : (const void*)k_sweep<G, S, false, false>;
-        static int grid = 0;
-        if (!grid) grid = grid_for(fn, 256, 0, ctx->sm_count);
-        const unsigned long long need = (g.nrows + 31) / 32;   // 32-row chunks, 8 warps per CTA
-        const int gr = (int)std::min<unsigned long long>(grid, (need + 7) / 8);
+        const bool exact = g.C == (unsigned)(G * S);
+        const bool w = ctx->weighted;
         if (dual) {
-            if (ctx->weighted) k_sweep<G, S, true, true><<<gr, 256, 0, ctx->stream>>>(b, g);
-            else k_sweep<G, S, true, false><<<gr, 256, 0, ctx->stream>>>(b, g);
-        } else {
-            if (ctx->weighted) k_sweep<G, S, false, true><<<gr, 256, 0, ctx->stream>>>(b, g);
-            else k_sweep<G, S, false, false><<<gr, 256, 0, ctx->stream>>>(b, g);
+            if (w) return exact ? launch_sweep_t<G, S, true, true, true>(ctx, b, g)
+                                : launch_sweep_t<G, S, true, true, false>(ctx, b, g);
+            return exact ? launch_sweep_t<G, S, true, false, true>(ctx, b, g)
+                         : launch_sweep_t<G, S, true, false, false>(ctx, b, g);
         }
-        ctx->launches++;
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_sweep launch: %s", cudaGetErrorString(e));
-        return FC_OK;
+        if (w) return exact ? launch_sweep_t<G, S, false, true, true>(ctx, b, g)
+                            : launch_sweep_t<G, S, false, true, false>(ctx, b, g);
+        return exact ? launch_sweep_t<G, S, false, false, true>(ctx, b, g)
+                     : launch_sweep_t<G, S, false, false, false>(ctx, b, g);
     }
 };
+
+template <int G, bool EXACT>
+int launch_step_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static int grid = 0;
+    const size_t smem = step_t_smem(G);
+    if (!grid) {
+        CU(cudaFuncSetAttribute(k_step_t<G, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_t<G, EXACT>, kStepThreads, smem, ctx->sm_count);
+    }
+    const unsigned long long need = (g.nrows + 32 * (kStepThreads / 32) - 1) / (32 * (kStepThreads / 32));
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
+    k_step_t<G, EXACT><<<gr, kStepThreads, smem, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_t launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
 
 template <int G, int S>
 struct LaunchStep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, int bt) {
         if (g.nrows == 0) return FC_OK;
+        if (S == 1 && !bt) {   // thread-per-row projection
+            return g.C == (unsigned)G ? launch_step_t<G, true>(ctx, b, g) : launch_step_t<G, false>(ctx, b, g);
+        }
         static int grid = 0;
         if (!grid) grid = grid_for((const void*)k_step<G, S>, 256, 0, ctx->sm_count);
         const unsigned long long need = (g.nrows + (32 / G) * 8 - 1) / ((32 / G) * 8);
@@ -291,6 +318,9 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
     if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
     if (c == 0) return set_err(ctx, FC_INVALID, "init_membership: dimensions must be positive");
     if (c > 256) return set_err(ctx, FC_INVALID, "cluster count C=%u exceeds the supported maximum 256", c);
+    if ((unsigned long long)ctx->n * c >= (1ULL << 32))
+        return set_err(ctx, FC_INVALID, "N*C = %llu exceeds 2^32 - 1 elements per membership replica",
+                       (unsigned long long)ctx->n * c);
     if (ctx->c == c && (!bt || ctx->bt_alloc)) return FC_OK;
     CU(cudaStreamSynchronize(ctx->stream));
     const size_t N = ctx->n, L = ctx->local_rows, LB = ctx->local_blocks;
@@ -426,8 +456,8 @@ int phase_rowsum(fc_ctx* ctx, int bt) {
 // broadcasts the final totals.
 int phase_combine(fc_ctx* ctx, int mat_mask, int scal_mask) {
     const size_t nch = nchains_of(ctx->c);
-    const int threads = 128;
-    const int blocks = (int)((nch + threads - 1) / threads);
+    const int threads = kCombThreads;
+    const int blocks = (int)((2 * npairs_of(ctx->c) + 31) / 32) + kNumScal;
     if (ctx->world == 1) {
         ProfScope p(ctx, kClsCombine);
         for (size_t s = 0; s < ctx->shards.size(); ++s) {

@@ -291,6 +291,21 @@ __device__ __forceinline__ double group_seq_sum(const double (&a)[S], int C) {
     return p;
 }
 
+// Same, restricted to one group's lanes (group-divergent code paths).
+template <int G, int S>
+__device__ __forceinline__ double group_seq_sum_m(const double (&a)[S], int C, unsigned gmask) {
+    double p = 0.0;
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) {
+#pragma unroll
+        for (int l2 = 0; l2 < G; ++l2) {
+            const double v = __shfl_sync(gmask, a[s2], l2, G);
+            if (s2 * G + l2 < C) p = dadd(p, v);
+        }
+    }
+    return p;
+}
+
 // =============================================================================
 // K1: CSR SpMM sweep with the loss-term epilogue.
 //   xs_i[r] = sum_{k in row i, ascending} w_k * X[j_k][r]      (objective.hpp:98-109)
@@ -300,74 +315,80 @@ __device__ __forceinline__ double group_seq_sum(const double (&a)[S], int C) {
 //   S bar^n                and   S X_ext^{n+1},  X_ext^{n+1}_j = bar_j + beta (bar_j - prev_j)
 // where each X_ext entry is formed exactly as solver.hpp:261 forms it, so both
 // sums are bit-identical to the reference's two separate sweeps.
-// Work: groups of G lanes own a row; warps pull 32-row chunks from a counter.
+// Work: groups of G lanes own a row (lane = component); warps pull 32-row
+// chunks from a counter (power-law rows balance dynamically).  The lane that
+// loads a column index pre-multiplies it by C (32-bit element offset, host
+// guarantees N*C < 2^32) and shuffles the offset; full G-wide index chunks
+// take a predicate-free path with U gathers (x2 when DUAL) in flight per lane.
+// EXACT: C == G*S (no idle lanes).
 // =============================================================================
-template <int G, int S, bool DUAL, bool W>
-__global__ void __launch_bounds__(256) k_sweep(Bufs b, Geo g) {
+template <int G, int S, bool DUAL, bool W, bool EXACT>
+__global__ void __launch_bounds__(256, 4) k_sweep(Bufs b, Geo g) {
     const DevState* st = b.st;
     if (st->done) return;
     constexpr int U = (G < 8) ? G : 8;
-    constexpr int RPW = 32 / G;           // rows per warp pass
-    constexpr unsigned kChunk = 32;       // rows per scheduler grab
-    const int C = (int)g.C;
-    const double* __restrict__ B = b.U[st->sw_b];
-    const double* __restrict__ P = DUAL ? b.U[st->sw_p] : nullptr;
-    const double beta = st->beta_next;
+    constexpr int RPW = 32 / G;
+    constexpr unsigned kChunk = 32;
+    const unsigned C = g.C;
     const unsigned lane = threadIdx.x & 31u;
-    const int lg = (int)(lane % G);
-    const int sub = (int)(lane / G);
-    double* xs_main = DUAL ? b.xs[st->xs_w * 2 + kMatBar] : b.xs[st->xs_w * 2 + kMatExt];
-    double* xs_ext = b.xs[st->xs_w * 2 + kMatExt];
+    const unsigned lg = lane % G;
+    const unsigned sub = lane / G;
+    const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (sub * G));
+    const double* __restrict__ B = b.U[st->sw_b] + lg;
+    const double* __restrict__ P = DUAL ? b.U[st->sw_p] + lg : nullptr;
+    const double beta = st->beta_next;
+    double* xs_main = (DUAL ? b.xs[st->xs_w * 2 + kMatBar] : b.xs[st->xs_w * 2 + kMatExt]) + lg;
+    double* xs_ext = b.xs[st->xs_w * 2 + kMatExt] + lg;
 
     for (;;) {
-        unsigned long long base = 0;
+        unsigned base = 0;
         if (lane == 0) base = atomicAdd(b.counter, kChunk);
         base = __shfl_sync(kFull, base, 0);
         if (base >= g.nrows) break;
-        for (unsigned off = 0; off < kChunk; off += RPW) {
-            const unsigned long long row = base + off + sub;
-            const bool active = row < g.nrows;
-            if (!__any_sync(kFull, active)) break;
-            long long e0 = 0, e1 = 0;
-            if (active) {
-                e0 = b.row_ptr[row];
-                e1 = b.row_ptr[row + 1];
-            }
+        const unsigned nr = (unsigned)min((unsigned long long)kChunk, g.nrows - base);
+        const long long rp = (lane <= nr) ? __ldg(b.row_ptr + base + lane) : 0;
+        const long long rp_end = __ldg(b.row_ptr + base + nr);
+        for (unsigned off = 0; off < nr; off += RPW) {
+            const unsigned rloc = off + sub;
+            const long long e0 = __shfl_sync(kFull, rp, rloc & 31u);
+            const long long e1n = __shfl_sync(kFull, rp, (rloc + 1) & 31u);
+            if (rloc >= nr) continue;                      // group-divergent from here on
+            const long long e1 = (rloc + 1 < 32) ? e1n : rp_end;
+            const unsigned long long row = base + rloc;
+            const size_t own = (size_t)(g.row0 + row) * C;
+            double xi[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) xi[s] = (EXACT || lg + s * G < C) ? ldg(B + own + s * G) : 0.0;
             double ab[S], ae[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) { ab[s] = 0.0; ae[s] = 0.0; }
 
-            for (long long eb = e0;; eb += G) {
-                const bool more = eb < e1;
-                if (!__any_sync(kFull, more)) break;
-                unsigned myj = 0;
+            for (long long eb = e0; eb < e1; eb += G) {
+                const int cnt = (int)min((long long)G, e1 - eb);
+                unsigned myoff = 0;
                 double myw = 1.0;
-                if (eb + lg < e1) {
-                    myj = __ldg(b.col + eb + lg);
+                if ((int)lg < cnt) {
+                    myoff = __ldg(b.col + eb + lg) * C;
                     if (W) myw = ldg(b.val + eb + lg);
                 }
-                const int cnt = more ? (int)min((long long)G, e1 - eb) : 0;
+                if (cnt == G) {
 #pragma unroll
-                for (int k0 = 0; k0 < G; k0 += U) {
-                    double vb[U][S];
-                    double vp[DUAL ? U : 1][S];
+                    for (int k0 = 0; k0 < G; k0 += U) {
+                        double vb[U][S];
+                        double vp[DUAL ? U : 1][S];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const unsigned j = __shfl_sync(kFull, myj, k0 + u, G);
-                        const bool ok = (k0 + u) < cnt;
+                        for (int u = 0; u < U; ++u) {
+                            const unsigned o = __shfl_sync(gmask, myoff, k0 + u, G);
 #pragma unroll
-                        for (int s = 0; s < S; ++s) {
-                            const int r = lg + s * G;
-                            const bool okc = ok && r < C;
-                            const size_t a = (size_t)j * (size_t)C + (size_t)r;
-                            vb[u][s] = okc ? ldg(B + a) : 0.0;
-                            if (DUAL) vp[u][s] = okc ? ldg(P + a) : 0.0;
+                            for (int s = 0; s < S; ++s) {
+                                const bool okc = EXACT || lg + s * G < C;
+                                vb[u][s] = okc ? ldg(B + o + s * G) : 0.0;
+                                if (DUAL) vp[u][s] = okc ? ldg(P + o + s * G) : 0.0;
+                            }
                         }
-                    }
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const double w = W ? __shfl_sync(kFull, myw, k0 + u, G) : 1.0;
-                        if ((k0 + u) < cnt) {
+                        for (int u = 0; u < U; ++u) {
+                            const double w = W ? __shfl_sync(gmask, myw, k0 + u, G) : 1.0;
 #pragma unroll
                             for (int s = 0; s < S; ++s) {
                                 ab[s] = W ? dadd(ab[s], dmul(w, vb[u][s])) : dadd(ab[s], vb[u][s]);
@@ -378,24 +399,49 @@ __global__ void __launch_bounds__(256) k_sweep(Bufs b, Geo g) {
                             }
                         }
                     }
+                } else {
+                    for (int k0 = 0; k0 < cnt; k0 += U) {
+                        double vb[U][S];
+                        double vp[DUAL ? U : 1][S];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const unsigned o = __shfl_sync(gmask, myoff, k0 + u, G);
+                            const bool ok = k0 + u < cnt;
+#pragma unroll
+                            for (int s = 0; s < S; ++s) {
+                                const bool okc = ok && (EXACT || lg + s * G < C);
+                                vb[u][s] = okc ? ldg(B + o + s * G) : 0.0;
+                                if (DUAL) vp[u][s] = okc ? ldg(P + o + s * G) : 0.0;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const double w = W ? __shfl_sync(gmask, myw, k0 + u, G) : 1.0;
+                            if (k0 + u < cnt) {
+#pragma unroll
+                                for (int s = 0; s < S; ++s) {
+                                    ab[s] = W ? dadd(ab[s], dmul(w, vb[u][s])) : dadd(ab[s], vb[u][s]);
+                                    if (DUAL) {
+                                        const double e = extrap(vb[u][s], vp[u][s], beta);
+                                        ae[s] = W ? dadd(ae[s], dmul(w, e)) : dadd(ae[s], e);
+                                    }
+                                }
+                            }
+                        }
+                    }
                 }
             }
-            // epilogue: store xs rows, prod_i
             double a[S];
-            const unsigned long long grow = g.row0 + row;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                const int r = lg + s * G;
-                a[s] = 0.0;
-                if (active && r < C) {
-                    const double xi = ldg(B + (size_t)grow * C + r);
-                    a[s] = dmul(ab[s], xi);
-                    xs_main[(size_t)row * C + r] = ab[s];
-                    if (DUAL) xs_ext[(size_t)row * C + r] = ae[s];
+                a[s] = dmul(ab[s], xi[s]);
+                if (EXACT || lg + s * G < C) {
+                    xs_main[(size_t)row * C + s * G] = ab[s];
+                    if (DUAL) xs_ext[(size_t)row * C + s * G] = ae[s];
                 }
             }
-            const double p = group_seq_sum<G, S>(a, C);
-            if (active && lg == 0) b.prod[row] = p;
+            const double pr = group_seq_sum_m<G, S>(a, (int)C, gmask);
+            if (lg == 0) b.prod[row] = pr;
         }
     }
 }
@@ -519,39 +565,91 @@ __global__ void __launch_bounds__(kGramThreads) k_gram(Bufs b, Geo g, int dual, 
 
 // =============================================================================
 // K4a: ordered combine of block partials (objective.hpp:82-88, :171):
-//   total = ((init + part_0) + part_1) + ...   one thread per chain.
-// Chains: [mat 0 pairs][mat 1 pairs][scalars].  `init` carries the running
-// total of the previous shard (multi-GPU ordered chain) or is null (0.0).
+//   total = ((init + part_0) + part_1) + ...
+// Chains: [mat 0 pairs][mat 1 pairs][scalars]; chain c's block-b partial is at
+// base_c + b * stride_c.  A CTA owns up to 32 chains: all its warps stage
+// [kCombTile blocks][32 chains] tiles into shared memory (coalesced: 32
+// consecutive pairs of one block are contiguous), and warp 0 (lane = chain)
+// adds them in ascending block order.  `init` carries the previous shard's
+// running totals (ordered multi-GPU chain) or is null (0.0).
+// grid.x = matrix-chain groups of 32, + one CTA per scalar chain.
 // =============================================================================
-__global__ void __launch_bounds__(128) k_combine(Bufs b, Geo g, int mat_mask, int scal_mask,
-                                                 const double* init) {
+constexpr int kCombTile = 64;
+constexpr int kCombThreads = 256;
+
+__global__ void __launch_bounds__(kCombThreads) k_combine(Bufs b, Geo g, int mat_mask, int scal_mask,
+                                                          const double* init) {
     if (b.st->done) return;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ double tile[2][kCombTile][32];
     const int np = (int)g.npairs;
-    const double* src;
-    size_t stride;
-    if (t < 2 * np) {
-        const int m = t / np;
-        if (!((mat_mask >> m) & 1)) return;
-        src = b.gpart[m] + (t % np);
-        stride = np;
+    const int mat_groups = (2 * np + 31) / 32;
+    const double* base;
+    int c0, nch;
+    if ((int)blockIdx.x < mat_groups) {
+        c0 = blockIdx.x * 32;
+        nch = min(32, 2 * np - c0);
+        // a group may straddle the two matrices: handle per chain below
+        base = nullptr;
     } else {
-        const int s = t - 2 * np;
+        const int s = blockIdx.x - mat_groups;
         if (s >= kNumScal || !((scal_mask >> s) & 1)) return;
-        src = b.spart + (size_t)s * g.spart_stride;
-        stride = 1;
+        c0 = 2 * np + s;
+        nch = 1;
+        base = b.spart + (size_t)s * g.spart_stride;
     }
-    double acc = init ? init[t] : 0.0;
-    unsigned long long k = 0;
-    for (; k + 8 <= g.nblk; k += 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = src[(k + u) * stride];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = dadd(acc, v[u]);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // per-chain source pointer (matrix chains)
+    auto src = [&](int c, unsigned long long blk) -> double {
+        if (base) return base[blk];
+        const int m = c / np;
+        return b.gpart[m][blk * (size_t)np + (c % np)];
+    };
+    const int my_c = c0 + lane;
+    bool live = lane < nch;
+    if (!base && live) live = (mat_mask >> (my_c / np)) & 1;
+    double acc = (live && init) ? init[my_c] : 0.0;
+    const unsigned long long nb = g.nblk;
+    const unsigned long long ntiles = (nb + kCombTile - 1) / kCombTile;
+    // stage tile 0
+    auto stage = [&](int buf, unsigned long long t) {
+        const unsigned long long b0 = t * kCombTile;
+        for (int e = threadIdx.x; e < kCombTile * 32; e += kCombThreads) {
+            const int r = e >> 5, c = e & 31;
+            const unsigned long long blk = b0 + r;
+            double v = 0.0;
+            if (blk < nb && c < nch) {
+                const int cc = c0 + c;
+                if (base || ((mat_mask >> (cc / np)) & 1)) v = src(cc, blk);
+            }
+            tile[buf][r][c] = v;
+        }
+    };
+    if (ntiles) stage(0, 0);
+    __syncthreads();
+    for (unsigned long long t = 0; t < ntiles; ++t) {
+        const int buf = (int)(t & 1);
+        if (warp == 0) {
+            const unsigned long long b0 = t * kCombTile;
+            const int rows = (int)min((unsigned long long)kCombTile, nb - b0);
+            if (live)
+                for (int r = 0; r < rows; ++r) acc = dadd(acc, tile[buf][r][lane]);
+        } else if (t + 1 < ntiles) {
+            // warps 1.. stage the next tile while warp 0 adds
+            const unsigned long long b0 = (t + 1) * kCombTile;
+            for (int e = threadIdx.x - 32; e < kCombTile * 32; e += kCombThreads - 32) {
+                const int r = e >> 5, c = e & 31;
+                const unsigned long long blk = b0 + r;
+                double v = 0.0;
+                if (blk < nb && c < nch) {
+                    const int cc = c0 + c;
+                    if (base || ((mat_mask >> (cc / np)) & 1)) v = src(cc, blk);
+                }
+                tile[buf ^ 1][r][c] = v;
+            }
+        }
+        __syncthreads();
     }
-    for (; k < g.nblk; ++k) acc = dadd(acc, src[k * stride]);
-    b.totals[t] = acc;
+    if (warp == 0 && live) b.totals[my_c] = acc;
 }
 
 __device__ __forceinline__ double packed_at(const double* tot, int r, int s, int C) {
@@ -849,6 +947,229 @@ __global__ void k_stamp(DevState* st) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     st->t0_ns = now;
 }
+
+// =============================================================================
+// Thread-per-row projection (simplex.hpp:18-59) for C <= CP <= 32: the row's
+// C values live in registers, so the reference's sequential loops (cumsum,
+// residual sums, max, ties) cost C instructions per THREAD instead of C per
+// warp and row.  Same operations in the same order as the reference.
+// =============================================================================
+template <int CP>
+__device__ __forceinline__ void bitonic_desc(double (&v)[CP]) {
+#pragma unroll
+    for (int k = 2; k <= CP; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < CP; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const double a = v[i], b = v[l];
+                    const bool sw = ((i & k) == 0) ? (a < b) : (b < a);
+                    v[i] = sw ? b : a;
+                    v[l] = sw ? a : b;
+                }
+            }
+        }
+    }
+}
+
+// cond_k of simplex.hpp:36: sorted_k - RN(a / d) >= 0, with a = RN(cs_k - 1),
+// d = k + 1.  Decided from RN(s*d) when it is clear of the rounding band
+// (|RN(s d) - s d| <= eps |s d|, d ulp(s)/2 <= eps |s d|: an 8 eps margin is
+// conservative), otherwise by the exact IEEE division the reference performs.
+__device__ __forceinline__ bool threshold_cond(double s, double a, double d) {
+    const double p = dmul(s, d);
+    const double mag = fmax(fabs(a), fabs(p));
+    if (mag >= 0x1p-900 && mag <= 0x1p+1000) {
+        const double margin = dmul(mag, 0x1p-50);
+        if (p >= dadd(a, margin)) return true;
+        if (p <= dsub(a, margin)) return false;
+    }
+    return dsub(s, a / d) >= 0.0;
+}
+
+// Threshold of simplex.hpp:29-36 for the row stored at r[0..C) (shared
+// memory, index order); only the sorted copy is held in registers.
+template <int CP>
+__device__ __forceinline__ double row_threshold(const double* r, int C) {
+    double v[CP];
+#pragma unroll
+    for (int k = 0; k < CP; ++k) v[k] = (k < C) ? r[k] : -INFINITY;
+    bitonic_desc<CP>(v);
+    double cs = 0.0, a_star = 0.0;
+    int k_star = -1;
+#pragma unroll
+    for (int k = 0; k < CP; ++k) {
+        if (k < C) {
+            cs = dadd(cs, v[k]);
+            const double a = dsub(cs, 1.0);
+            if (threshold_cond(v[k], a, (double)(k + 1))) {
+                k_star = k;
+                a_star = a;
+            }
+        }
+    }
+    return k_star >= 0 ? a_star / (double)(k_star + 1) : 0.0;
+}
+
+template <int CP>
+__device__ __forceinline__ void fold_residual(double (&w)[CP], int C) {
+#pragma unroll 1
+    for (int round = 0; round < 4; ++round) {
+        double sum = 0.0;
+#pragma unroll
+        for (int k = 0; k < CP; ++k)
+            if (k < C) sum = dadd(sum, w[k]);
+        const double residual = dsub(sum, 1.0);
+        if (residual == 0.0) break;
+        double top = w[0];
+#pragma unroll
+        for (int k = 1; k < CP; ++k)
+            if (k < C) top = (top < w[k]) ? w[k] : top;
+        int ties = 0;
+#pragma unroll
+        for (int k = 0; k < CP; ++k)
+            if (k < C) ties += (w[k] == top);
+        const double share = residual / (double)ties;
+#pragma unroll
+        for (int k = 0; k < CP; ++k)
+            if (k < C && w[k] == top) w[k] = ref_max(dsub(w[k], share), 0.0);
+    }
+}
+
+// K3 (C <= 32, no backtracking terms).  Each warp handles batches of 32 rows
+// through ONE per-warp shared tile [32][G+1] (stride G+1: conflict-free
+// row-per-thread access):
+//   1a lane = component (coalesced): X_ext rows -> tile;  2a thread = row: x -> registers
+//   1b lane = component: S X_ext rows -> tile
+//   2b thread = row: g_k = -4 (xs_k - sum_l G[k][l] x_l)  (4 independent k chains,
+//      G broadcast from shared memory as double2), y_k = x_k - tau g_k,
+//      projection -- all in the reference's operation order
+//   3  lane = component: coalesced store of bar^n.
+// G (power of two, 2..32) is the padded row width, C <= G; EXACT: C == G.
+constexpr int kStepThreads = 128;
+
+template <int G, bool EXACT>
+__global__ void __launch_bounds__(kStepThreads, 4) k_step_t(Bufs b, Geo g) {
+    DevState* st = b.st;
+    if (st->done) return;
+    extern __shared__ double smt[];
+    constexpr int LD = G + 1;
+    constexpr int RPW = 32 / G;
+    constexpr int KU = G < 4 ? G : 4;
+    const int C = EXACT ? G : (int)g.C;
+    const unsigned lane = threadIdx.x & 31u;
+    const int lg = (int)(lane % G);
+    const int sub = (int)(lane / G);
+    const int warp = threadIdx.x >> 5;
+    double* Gr = smt;                                        // Gr[k*G + l] = G[k][l]
+    double* T = smt + G * G + warp * 32 * LD;
+    const int mode = st->step_mode;
+    const double* __restrict__ A = b.U[st->step_a];
+    const double* __restrict__ Bp = b.U[st->step_b];
+    double* __restrict__ D = b.U[st->step_dst];
+    const double beta = st->beta_step;
+    const double tau = st->tau;
+    const int sel = st->step_sel;
+    const double* __restrict__ XS = b.xs[st->xs_r * 2 + sel];
+    const double* __restrict__ Gt = b.gfull[sel];            // Gt[l*C + k] == G[k][l]
+    for (int e = threadIdx.x; e < G * G; e += blockDim.x) {
+        const int k = e / G, l = e % G;
+        Gr[e] = (k < C && l < C) ? Gt[l * C + k] : 0.0;
+    }
+    __syncthreads();
+
+    const unsigned long long warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    const bool lane_ok = EXACT || lg < C;
+    double* Tr = T + lane * LD;                              // this thread's row in phase 2
+    bool bad = false;
+    for (unsigned long long rb = w0 * 32; rb < g.nrows; rb += warps * 32) {
+        const bool row_ok = rb + lane < g.nrows;
+        // 1a: x rows
+#pragma unroll 4
+        for (int p = 0; p < 32; p += RPW) {
+            const unsigned long long row = rb + p + sub;
+            if (row < g.nrows && lane_ok) {
+                const size_t a = (size_t)(g.row0 + row) * C + lg;
+                const double av = A[a];
+                T[(p + sub) * LD + lg] = (mode == kLiteral) ? av : extrap(av, Bp[a], beta);
+            }
+        }
+        __syncwarp();
+        double xr[G];
+#pragma unroll
+        for (int l = 0; l < G; ++l) xr[l] = (EXACT || l < C) ? Tr[l] : 0.0;
+        __syncwarp();
+        // 1b: xs rows
+#pragma unroll 4
+        for (int p = 0; p < 32; p += RPW) {
+            const unsigned long long row = rb + p + sub;
+            if (row < g.nrows && lane_ok) T[(p + sub) * LD + lg] = XS[(size_t)row * C + lg];
+        }
+        __syncwarp();
+        if (row_ok) {
+            // 2b: gradient (objective.hpp:37-43, :116-117), KU independent chains
+#pragma unroll 1
+            for (int k0 = 0; k0 < C; k0 += KU) {
+                double o[KU];
+#pragma unroll
+                for (int u = 0; u < KU; ++u) o[u] = 0.0;
+#pragma unroll
+                for (int l2 = 0; l2 < G / 2; ++l2) {
+#pragma unroll
+                    for (int u = 0; u < KU; ++u) {
+                        const double2 gg = reinterpret_cast<const double2*>(Gr + (k0 + u) * G)[l2];
+                        if (EXACT || 2 * l2 < C) o[u] = dadd(o[u], dmul(gg.x, xr[2 * l2]));
+                        if (EXACT || 2 * l2 + 1 < C) o[u] = dadd(o[u], dmul(gg.y, xr[2 * l2 + 1]));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < KU; ++u)
+                    if (EXACT || k0 + u < C) Tr[k0 + u] = dmul(-4.0, dsub(Tr[k0 + u], o[u]));
+            }
+            // y = x - tau * grad (solver.hpp:102)
+            bool fin = true;
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                if (EXACT || k < C) {
+                    const double y = dsub(xr[k], dmul(tau, Tr[k]));
+                    fin = fin && isfinite(y);
+                    Tr[k] = y;
+                }
+            }
+            if (!fin) {
+                bad = true;
+            } else if (C == 1) {
+                Tr[0] = 1.0;
+            } else {
+                const double thr = row_threshold<G>(Tr, C);
+                double w[G];
+#pragma unroll
+                for (int k = 0; k < G; ++k) w[k] = (EXACT || k < C) ? ref_max(dsub(Tr[k], thr), 0.0) : 0.0;
+                fold_residual<G>(w, C);
+#pragma unroll
+                for (int k = 0; k < G; ++k)
+                    if (EXACT || k < C) Tr[k] = w[k];
+            }
+        }
+        __syncwarp();
+        // 3: store bar^n
+#pragma unroll 4
+        for (int p = 0; p < 32; p += RPW) {
+            const unsigned long long r2 = rb + p + sub;
+            if (r2 < g.nrows && lane_ok) D[(size_t)(g.row0 + r2) * C + lg] = T[(p + sub) * LD + lg];
+        }
+        __syncwarp();
+    }
+    if (bad) {
+        st->error = 1;
+        st->done = 1;
+    }
+}
+
+inline size_t step_t_smem(int G) { return sizeof(double) * ((size_t)G * G + (kStepThreads / 32) * 32 * (G + 1)); }
 
 // Batched in-place projection (init_membership's per-column projection).
 template <int G, int S>
