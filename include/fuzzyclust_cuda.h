@@ -5,7 +5,7 @@
  * The reference (arXiv 2506.04045, /root/reference/proj) is a header-only C++
  * library with no FFI; its "operator API" is the inline header API that callers
  * #include (fuzzyclust.hpp:1-14).  This ABI is what those header bodies bind to
- * (see include/fuzzyclust/*.hpp and INTEGRATION.md).  Each entry point names the
+ * (see the headers under include/fuzzyclust/ and INTEGRATION.md).  Each entry point names the
  * reference interface it replaces.
  *
  * Conventions:
@@ -118,6 +118,15 @@ int fc_gpa_step(fc_ctx* ctx, uint32_t c, const double* x, const double* g, doubl
 /* project_simplex_inplace (simplex.hpp:18-59) applied to `rows` vectors of
  * length c stored contiguously (init_membership's per-column projection). */
 int fc_project_simplex_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, double* x);
+
+/* Per-row pieces used by the reference's single-column API (host buffers):
+ *   gradient_column_fused (objective.hpp:113-118): out_i = -4 (xs_i - G x_i)
+ *   loss_terms_column     (objective.hpp:131-135): out_i = sum_k xs_i[k] x_i[k]
+ * g is C x C row-major; xs, x, out are `rows` vectors of length c. */
+int fc_gradient_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, const double* g, const double* xs,
+                     const double* x, double* out);
+int fc_loss_terms_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, const double* xs, const double* x,
+                       double* out);
 
 /* ---- solver ---------------------------------------------------------------
  * solve / run_gpa / run_fista, solver.hpp:137-277: the whole loop on device.

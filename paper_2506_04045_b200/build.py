@@ -57,5 +57,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+DROPIN_SRC = os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp")
+DROPIN_BIN = os.path.join(ROOT, "tests", "cpp", "_build", "dropin_test")
+
+
+def build_dropin_test(force: bool = False) -> str:
+    """C++ caller of the drop-in headers (include/fuzzyclust/*.hpp) linked to the library."""
+    deps = [DROPIN_SRC, LIB] + [os.path.join(ROOT, "include", "fuzzyclust", f)
+                                for f in os.listdir(os.path.join(ROOT, "include", "fuzzyclust"))]
+    if not force and os.path.exists(DROPIN_BIN) and all(os.path.getmtime(p) <= os.path.getmtime(DROPIN_BIN)
+                                                         for p in deps):
+        return DROPIN_BIN
+    os.makedirs(os.path.dirname(DROPIN_BIN), exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I" + os.path.join(ROOT, "include"),
+           "-I" + os.path.dirname(DROPIN_SRC), DROPIN_SRC, "-L" + LIBDIR, "-lfuzzyclust_cuda",
+           "-Wl,-rpath," + LIBDIR, "-o", DROPIN_BIN]
+    subprocess.run(cmd, check=True)
+    return DROPIN_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

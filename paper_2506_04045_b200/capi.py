@@ -63,6 +63,8 @@ SIGNATURES = {
     "fc_gpa_step_fused": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp, C.c_double, _dp]),
     "fc_gpa_step": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, C.c_double, _dp]),
     "fc_project_simplex_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, _dp]),
+    "fc_gradient_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, _dp, _dp, _dp, _dp]),
+    "fc_loss_terms_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, _dp, _dp, _dp]),
     "fc_solve": (C.c_int, [C.c_void_p, C.POINTER(SolverConfigC), C.c_uint32, _dp, _dp,
                            C.POINTER(TraceRecordC), C.c_uint64, C.POINTER(SummaryC)]),
     "fc_solver_begin": (C.c_int, [C.c_void_p, C.POINTER(SolverConfigC), C.c_uint32, _dp]),
@@ -234,6 +236,22 @@ class Context:
             y = y.reshape(1, -1)
         self._c(lib().fc_project_simplex_rows(self.h, y.shape[1], y.shape[0], _p(y)))
         return y
+
+    def gradient_rows(self, g, xs, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        x2 = x.reshape(-1, x.shape[-1])
+        out = np.empty_like(x2)
+        self._c(lib().fc_gradient_rows(self.h, x2.shape[1], x2.shape[0], _p(np.ascontiguousarray(g, dtype=np.float64)),
+                                       _p(np.ascontiguousarray(xs, dtype=np.float64).reshape(x2.shape)), _p(x2), _p(out)))
+        return out.reshape(x.shape)
+
+    def loss_terms_rows(self, xs, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        x2 = x.reshape(-1, x.shape[-1])
+        out = np.empty(x2.shape[0])
+        self._c(lib().fc_loss_terms_rows(self.h, x2.shape[1], x2.shape[0],
+                                         _p(np.ascontiguousarray(xs, dtype=np.float64).reshape(x2.shape)), _p(x2), _p(out)))
+        return out
 
     # ---- solver -------------------------------------------------------------
     @staticmethod

@@ -918,6 +918,43 @@ int fc_project_simplex_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, double* x) {
     return FC_OK;
 }
 
+static int rows_kernel(fc_ctx* ctx, uint32_t c, uint64_t rows, const double* g, const double* xs,
+                       const double* x, double* out, bool gradient) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    if (c == 0) return set_err(ctx, FC_INVALID, "objective: empty column");
+    if (rows == 0) return FC_OK;
+    CU(cudaSetDevice(ctx->device));
+    const size_t vb = rows * c * sizeof(double);
+    const size_t gb = gradient ? (size_t)c * c * sizeof(double) : 0;
+    const size_t ob = gradient ? vb : rows * sizeof(double);
+    char* d = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&d), gb + 2 * vb + ob, ctx->stream));
+    double* dg = reinterpret_cast<double*>(d);
+    double* dxs = reinterpret_cast<double*>(d + gb);
+    double* dx = reinterpret_cast<double*>(d + gb + vb);
+    double* dout = reinterpret_cast<double*>(d + gb + 2 * vb);
+    if (gradient) TRY(h2d(ctx, dg, g, gb));
+    TRY(h2d(ctx, dxs, xs, vb));
+    TRY(h2d(ctx, dx, x, vb));
+    const unsigned blocks = (unsigned)((rows + 127) / 128);
+    if (gradient) k_gradient_rows<<<blocks, 128, 0, ctx->stream>>>(dg, dxs, dx, dout, rows, (int)c);
+    else k_loss_terms_rows<<<blocks, 128, 0, ctx->stream>>>(dxs, dx, dout, rows, (int)c);
+    TRY(check_launch(ctx, gradient ? "k_gradient_rows" : "k_loss_terms_rows"));
+    TRY(d2h(ctx, out, dout, ob));
+    CU(cudaFreeAsync(d, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return FC_OK;
+}
+
+int fc_gradient_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, const double* g, const double* xs, const double* x,
+                     double* out) {
+    return rows_kernel(ctx, c, rows, g, xs, x, out, true);
+}
+
+int fc_loss_terms_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, const double* xs, const double* x, double* out) {
+    return rows_kernel(ctx, c, rows, nullptr, xs, x, out, false);
+}
+
 // ---- solver --------------------------------------------------------------------------
 int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const double* x0) {
     if (!ctx) return set_err(nullptr, FC_INVALID, "null context");

@@ -941,6 +941,30 @@ __global__ void __launch_bounds__(256) k_step(Bufs b, Geo g, int bt) {
     }
 }
 
+// Row-wise gradient / loss term for the single-column API (not on the
+// iteration path): one thread per row, the reference's loops verbatim.
+__global__ void k_gradient_rows(const double* g, const double* xs, const double* x, double* out,
+                                unsigned long long rows, int C) {
+    const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const double* xi = x + i * C;
+    const double* xsi = xs + i * C;
+    double* o = out + i * C;
+    for (int k = 0; k < C; ++k) {
+        double acc = 0.0;
+        for (int l = 0; l < C; ++l) acc = dadd(acc, dmul(g[k * C + l], xi[l]));
+        o[k] = dmul(-4.0, dsub(xsi[k], acc));
+    }
+}
+
+__global__ void k_loss_terms_rows(const double* xs, const double* x, double* out, unsigned long long rows, int C) {
+    const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    double acc = 0.0;
+    for (int k = 0; k < C; ++k) acc = dadd(acc, dmul(xs[i * C + k], x[i * C + k]));
+    out[i] = acc;
+}
+
 // Device clock origin of TraceRecord::elapsed_ms.
 __global__ void k_stamp(DevState* st) {
     long long now;
