@@ -15,6 +15,8 @@
 //   k_rowsum  per-block merge partials
 //   k_combine ordered block combine (cross-shard: ordered NCCL send/recv chain)
 //   k_finalize loss, stop rule, trace record, plan of iteration n+1
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -96,6 +98,10 @@ struct fc_ctx {
     uint64_t enqueued = 0;             // iterations enqueued after begin
     uint64_t host_iter = 0;            // FISTA/GPA iteration index of the next enqueued pass
     cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
+
+    bool sweep_tma = false;            // FC_SWEEP=tma selects the TMA gather4 sweep
+    bool umaps_ok = false;
+    UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
 
     // profiling
     bool profiling = false;
@@ -228,10 +234,32 @@ int launch_sweep_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     return FC_OK;
 }
 
+template <int S, bool DUAL>
+int launch_sweep_tma(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static int grid = 0;
+    const size_t smem = sweep_tma_smem((int)g.C, DUAL ? 1 : 0);
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        CU(cudaFuncSetAttribute(k_sweep_tma<S, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+        grid = grid_for((const void*)k_sweep_tma<S, DUAL>, kSwTmaThreads, smem, ctx->sm_count);
+    }
+    const unsigned long long need = (g.nrows + 31) / 32;
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, (need + 3) / 4));
+    k_sweep_tma<S, DUAL><<<gr, kSwTmaThreads, smem, ctx->stream>>>(b, g, ctx->umaps);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_sweep_tma launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
 template <int G, int S>
 struct LaunchSweep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, bool dual) {
         if (g.nrows == 0) return FC_OK;
+        if (G == 32 && g.C > 16 && (g.C % 4) == 0 && !ctx->weighted && ctx->sweep_tma && ctx->umaps_ok) {
+            return dual ? launch_sweep_tma<S, true>(ctx, b, g) : launch_sweep_tma<S, false>(ctx, b, g);
+        }
         const bool exact = g.C == (unsigned)(G * S);
         const bool w = ctx->weighted;
         if (dual) {
@@ -310,8 +338,35 @@ size_t nchains_of(uint32_t c) { return 2 * (size_t)npairs_of(c) + kNumScal; }
 
 int gram_rows_per_chunk(uint32_t c) {
     const int c4 = (int)((c + 3) & ~3u);
-    int r = 2048 / c4;
-    return std::max(4, std::min(64, r));
+    return std::max(4, std::min(32, 1024 / c4));
+}
+
+// Tensor maps for the TMA gather4 sweep: U[k] as a 2-D [N][C] f64 tensor, box {C, 1}.
+int make_umaps(fc_ctx* ctx) {
+    ctx->umaps_ok = false;
+    const uint32_t c = ctx->c;
+    if (c <= 16 || c > 256 || (c % 4)) return FC_OK;   // gather4 destinations: 4*8C bytes, 128-B aligned
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return FC_OK;                                    // TMA variant unavailable: LDG sweep is used
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    for (int k = 0; k < 3; ++k) {
+        const cuuint64_t dims[2] = {c, ctx->n};
+        const cuuint64_t strides[1] = {(cuuint64_t)c * sizeof(double)};
+        const cuuint32_t box[2] = {c, 1};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode(&ctx->umaps.m[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ctx->d_U[k], dims, strides,
+                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return FC_OK;
+    }
+    ctx->umaps_ok = true;
+    return FC_OK;
 }
 
 int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
@@ -344,6 +399,7 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
     CU(cudaMemsetAsync(ctx->d_totals, 0, (ctx->vshards + 1) * nchains_of(c) * sizeof(double), ctx->stream));
     ctx->c = c;
     ctx->bt_alloc = bt;
+    TRY(make_umaps(ctx));
     return FC_OK;
 }
 
@@ -407,7 +463,7 @@ int phase_gram(fc_ctx* ctx, bool dual) {
     const int nT = c4 / 4;
     const int tiles = nT * (nT + 1) / 2 * (dual ? 2 : 1);
     const int R = gram_rows_per_chunk(c);
-    const size_t smem = (size_t)(dual ? 2 : 1) * R * c4 * sizeof(double);
+    const size_t smem = gram_smem((int)c, dual ? 1 : 0, R);
     static size_t smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
         CU(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -464,7 +520,7 @@ int phase_combine(fc_ctx* ctx, int mat_mask, int scal_mask) {
             const Bufs b = make_bufs(ctx, s);
             const Geo g = make_geo(ctx, s);
             const double* init = s == 0 ? nullptr : ctx->d_totals + (s - 1) * nch;
-            k_combine<<<blocks, threads, 0, ctx->stream>>>(b, g, mat_mask, scal_mask, init);
+            k_combine<<<blocks, threads, kCombSmem, ctx->stream>>>(b, g, mat_mask, scal_mask, init);
             TRY(check_launch(ctx, "k_combine"));
         }
         return FC_OK;
@@ -477,7 +533,7 @@ int phase_combine(fc_ctx* ctx, int mat_mask, int scal_mask) {
         ProfScope p(ctx, kClsCombine);
         const Bufs b = make_bufs(ctx, 0);
         const Geo g = make_geo(ctx, 0);
-        k_combine<<<blocks, threads, 0, ctx->stream>>>(b, g, mat_mask, scal_mask,
+        k_combine<<<blocks, threads, kCombSmem, ctx->stream>>>(b, g, mat_mask, scal_mask,
                                                        ctx->rank > 0 ? ctx->d_chain_in : nullptr);
         TRY(check_launch(ctx, "k_combine"));
     }
@@ -647,6 +703,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         return set_err(ctx, FC_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a (B200)", device,
                        prop.major, prop.minor);
     ctx->sm_count = prop.multiProcessorCount;
+    if (const char* sw = std::getenv("FC_SWEEP")) ctx->sweep_tma = std::strcmp(sw, "tma") == 0;
     CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CU(cudaMalloc(&ctx->d_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_state, sizeof(DevState)));
@@ -660,6 +717,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         NC(ncclCommInitRank(&ctx->comm, world, u, rank));
     }
     TRY(ensure_trace(ctx, 1024));
+    CU(cudaFuncSetAttribute(k_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCombSmem));
     return FC_OK;
 }
 

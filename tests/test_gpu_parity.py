@@ -264,3 +264,21 @@ def test_large_sbm_properties(ctx):
     # and the device run is deterministic
     r2 = ctx.solve(x0, cfg(method=FISTA, max_iter=6, fista_restart=True))
     assert np.array_equal(r2["membership"], x) and recs(r2) == recs(r)
+
+
+# ---- the TMA gather4 sweep variant (FC_SWEEP=tma) ------------------------------------------------
+@pytest.mark.parametrize("n,c", [(3000, 20), (5000, 32), (2100, 64), (1500, 128)])
+def test_tma_sweep_variant_bitwise(oracle, n, c, monkeypatch):
+    monkeypatch.setenv("FC_SWEEP", "tma")
+    t = capi.Context(0)
+    try:
+        g = random_graph(n, 9.0, n + c)
+        t.upload(g)
+        x0 = oracle.init_random(n, c, 2)
+        for kw in [dict(method=GPA, max_iter=12), dict(method=FISTA, max_iter=12, fista_restart=True)]:
+            assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+        xs, m = t.fused_column_pass(x0)
+        xs_o, m_o = oracle.fused_column_pass(x0, g)
+        assert np.array_equal(xs, xs_o) and m == m_o
+    finally:
+        t.close()
