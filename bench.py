@@ -302,6 +302,7 @@ def main():
         barrier(world)
         t0 = time.perf_counter()
         ctx.upload(graph)                              # CSR H2D (shard)
+        tu = time.perf_counter()
         r = ctx.solve(x0, ecfg, want_x=True)           # x0 H2D, solve, membership + trace D2H
         t1 = time.perf_counter()
         e_local = t1 - t0
@@ -312,7 +313,8 @@ def main():
         d2h = 8 * graph.n * cfg["c"] + 40 * len(r["records"])
         e2e = {"value": r["iterations"] / e_s, "unit": "iter/s", "h2d_bytes_per_step": int(h2d / max(1, r["iterations"])),
                "d2h_bytes_per_step": int(d2h / max(1, r["iterations"])), "seconds": e_s,
-               "iterations": r["iterations"], "includes": "CSR upload + x0 H2D + prelude + solve + result D2H"}
+               "iterations": r["iterations"], "upload_s": tu - t0, "solve_call_s": t1 - tu,
+               "includes": "CSR upload + x0 H2D + prelude + solve + result D2H"}
 
     # ---- roofline of the dominant kernel (k_sweep) -----------------------------------------
     peak, peak_kind = peaks()

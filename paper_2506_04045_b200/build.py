@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
-LIB = os.path.join(LIBDIR, "libfuzzyclust_cuda.so")
+LIB = os.environ.get("FC_LIB") or os.path.join(LIBDIR, "libfuzzyclust_cuda.so")
 SOURCES = [os.path.join(CSRC, "fc_capi.cu"), os.path.join(CSRC, "generator.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "fc_kernels.cuh"), os.path.join(ROOT, "include", "fuzzyclust_cuda.h")]
 

@@ -22,12 +22,15 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "fc_kernels.cuh"
@@ -41,6 +44,22 @@ using namespace fc;
 namespace {
 
 thread_local std::string g_thread_err;
+
+// FC_TRACE_HOST=1: print host-side phase timings (stderr).
+struct HostPhase {
+    const char* name;
+    std::chrono::steady_clock::time_point t0;
+    static bool on() {
+        static const bool v = [] { const char* e = std::getenv("FC_TRACE_HOST"); return e && *e == '1'; }();
+        return v;
+    }
+    explicit HostPhase(const char* n) : name(n), t0(std::chrono::steady_clock::now()) {}
+    ~HostPhase() {
+        if (on())
+            std::fprintf(stderr, "[fc] %-22s %8.2f ms\n", name,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
 
 struct Shard {
     uint64_t row0 = 0, nrows = 0;      // global rows [row0, row0 + nrows)
@@ -71,6 +90,10 @@ struct fc_ctx {
     long long* d_row_ptr = nullptr;
     unsigned* d_col = nullptr;
     double* d_val = nullptr;
+    uint64_t local_nnz = 0;
+    unsigned* d_deg = nullptr;         // degree of every node (hot-row selection)
+    std::vector<uint64_t> deg_hist;    // nodes per degree value
+    unsigned hot_threshold = 0xFFFFFFFFu;
 
     // work buffers
     uint32_t c = 0;
@@ -102,6 +125,15 @@ struct fc_ctx {
     bool sweep_tma = false;            // FC_SWEEP=tma selects the TMA gather4 sweep
     bool umaps_ok = false;
     UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
+
+    // pinned staging ring for large host<->device copies
+    static constexpr int kStageBufs = 3;
+    static constexpr size_t kStageChunk = size_t(64) << 20;
+    char* stage_buf[kStageBufs] = {nullptr, nullptr, nullptr};
+    cudaEvent_t stage_ev[kStageBufs] = {nullptr, nullptr, nullptr};
+    int copy_threads = 8;
+
+    std::unordered_map<const void*, size_t> caps;   // device allocation capacities (bytes)
 
     // profiling
     bool profiling = false;
@@ -146,21 +178,28 @@ int set_err(fc_ctx* ctx, int code, const char* fmt, ...) {
         if (rc_) return rc_;       \
     } while (0)
 
+// Capacity-based device allocation: an existing buffer is reused whenever it is
+// large enough (cudaFree synchronizes the device and returns memory to the
+// driver, so re-uploads and new solves must not churn multi-GB allocations).
 template <class T>
 int dalloc(fc_ctx* ctx, T** p, size_t count) {
-    if (*p) {
-        cudaFree(*p);
-        *p = nullptr;
-    }
     if (count == 0) count = 1;
-    CU(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+    const size_t bytes = count * sizeof(T);
+    size_t& cap = ctx->caps[(const void*)p];
+    if (*p && cap >= bytes) return FC_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    cap = 0;
+    CU(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+    cap = bytes;
     return FC_OK;
 }
 
 template <class T>
-void dfree(T** p) {
+void dfree(fc_ctx* ctx, T** p) {
     if (*p) cudaFree(*p);
     *p = nullptr;
+    ctx->caps[(const void*)p] = 0;
 }
 
 // ---- kernel-class timing ------------------------------------------------------
@@ -369,6 +408,33 @@ int make_umaps(fc_ctx* ctx) {
     return FC_OK;
 }
 
+// Hot rows: the highest-degree nodes whose two gathered replicas (bar, prev)
+// fit the L2 budget FC_HOT_MB (default 0 = off) are loaded with an
+// L2::evict_last policy by k_sweep (flag = bit 31 of the stored column index).
+int set_hot_rows(fc_ctx* ctx) {
+    double mb = 0.0;
+    if (const char* e = std::getenv("FC_HOT_MB")) mb = std::atof(e);
+    unsigned thr = 0xFFFFFFFFu;
+    if (mb > 0.0 && !ctx->deg_hist.empty()) {
+        const double rows_budget = mb * 1e6 / (2.0 * 8.0 * ctx->c);
+        uint64_t cum = 0;
+        for (size_t d = ctx->deg_hist.size(); d-- > 1;) {
+            if ((double)(cum + ctx->deg_hist[d]) > rows_budget) break;
+            cum += ctx->deg_hist[d];
+            thr = (unsigned)d;
+        }
+    }
+    if (thr == ctx->hot_threshold) return FC_OK;
+    const unsigned long long nnz = ctx->local_nnz;
+    if (nnz) {
+        const unsigned blocks = (unsigned)std::min<unsigned long long>((nnz + 255) / 256, (unsigned long long)ctx->sm_count * 16);
+        k_flag_hot<<<blocks, 256, 0, ctx->stream>>>(ctx->d_col, nnz, ctx->d_deg, thr);
+        TRY(check_launch(ctx, "k_flag_hot"));
+    }
+    ctx->hot_threshold = thr;
+    return FC_OK;
+}
+
 int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
     if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
     if (c == 0) return set_err(ctx, FC_INVALID, "init_membership: dimensions must be positive");
@@ -383,12 +449,10 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
     for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_xs[k], L * c));
     for (int k = 2; k < 4; ++k) {
         if (bt) TRY(dalloc(ctx, &ctx->d_xs[k], L * c));
-        else dfree(&ctx->d_xs[k]);
     }
     TRY(dalloc(ctx, &ctx->d_prod, L));
     for (int k = 0; k < 3; ++k) {
         if (bt) TRY(dalloc(ctx, &ctx->d_rowterm[k], L));
-        else dfree(&ctx->d_rowterm[k]);
     }
     const unsigned np = npairs_of(c);
     for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_gpart[k], LB * np));
@@ -400,6 +464,7 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
     ctx->c = c;
     ctx->bt_alloc = bt;
     TRY(make_umaps(ctx));
+    TRY(set_hot_rows(ctx));
     return FC_OK;
 }
 
@@ -633,6 +698,76 @@ int d2h(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
     return FC_OK;
 }
 
+// ---- large host<->device copies through a pinned staging ring ----------------------
+// Pageable cudaMemcpy moves data through one driver thread; here the host side
+// of each 64 MB chunk is copied by several threads into pinned memory while the
+// previous chunk's DMA runs.
+void par_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+    if (threads <= 1 || bytes < (size_t(4) << 20)) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t part = (bytes + threads - 1) / threads;
+    for (int t = 0; t < threads; ++t) {
+        const size_t a = std::min(bytes, (size_t)t * part), b = std::min(bytes, a + part);
+        if (b > a) pool.emplace_back([=] { std::memcpy((char*)dst + a, (const char*)src + a, b - a); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+int ensure_staging(fc_ctx* ctx) {
+    for (int k = 0; k < fc_ctx::kStageBufs; ++k) {
+        if (!ctx->stage_buf[k]) CU(cudaMallocHost(reinterpret_cast<void**>(&ctx->stage_buf[k]), fc_ctx::kStageChunk));
+        if (!ctx->stage_ev[k]) CU(cudaEventCreateWithFlags(&ctx->stage_ev[k], cudaEventDisableTiming));
+    }
+    return FC_OK;
+}
+
+// Returns once `src` has been consumed (the DMA may still be in flight, stream-ordered).
+int h2d_big(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes < (size_t(8) << 20)) return h2d(ctx, dst, src, bytes);
+    TRY(ensure_staging(ctx));
+    const size_t ch = fc_ctx::kStageChunk;
+    int k = 0;
+    for (size_t off = 0; off < bytes; off += ch, k = (k + 1) % fc_ctx::kStageBufs) {
+        const size_t n = std::min(ch, bytes - off);
+        CU(cudaEventSynchronize(ctx->stage_ev[k]));           // buffer k's previous DMA has finished
+        par_memcpy(ctx->stage_buf[k], (const char*)src + off, n, ctx->copy_threads);
+        CU(cudaMemcpyAsync((char*)dst + off, ctx->stage_buf[k], n, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaEventRecord(ctx->stage_ev[k], ctx->stream));
+    }
+    return FC_OK;
+}
+
+// Synchronous: `dst` holds the data on return.
+int d2h_big(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes < (size_t(8) << 20)) {
+        TRY(d2h(ctx, dst, src, bytes));
+        CU(cudaStreamSynchronize(ctx->stream));
+        return FC_OK;
+    }
+    TRY(ensure_staging(ctx));
+    const size_t ch = fc_ctx::kStageChunk;
+    const size_t nchunks = (bytes + ch - 1) / ch;
+    auto issue = [&](size_t i) -> int {
+        const int k = (int)(i % fc_ctx::kStageBufs);
+        const size_t off = i * ch, n = std::min(ch, bytes - off);
+        CU(cudaMemcpyAsync(ctx->stage_buf[k], (const char*)src + off, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaEventRecord(ctx->stage_ev[k], ctx->stream));
+        return FC_OK;
+    };
+    for (size_t i = 0; i < nchunks && i < (size_t)fc_ctx::kStageBufs; ++i) TRY(issue(i));
+    for (size_t i = 0; i < nchunks; ++i) {
+        const int k = (int)(i % fc_ctx::kStageBufs);
+        const size_t off = i * ch, n = std::min(ch, bytes - off);
+        CU(cudaEventSynchronize(ctx->stage_ev[k]));
+        par_memcpy((char*)dst + off, ctx->stage_buf[k], n, ctx->copy_threads);
+        if (i + fc_ctx::kStageBufs < nchunks) TRY(issue(i + fc_ctx::kStageBufs));
+    }
+    return FC_OK;
+}
+
 // x0.validate(1e-9) on the device (membership.hpp:49-61); x already in U[buf]
 int validate_x(fc_ctx* ctx, int buf, double tol) {
     DevState s = base_state(ctx);
@@ -704,6 +839,11 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
                        prop.major, prop.minor);
     ctx->sm_count = prop.multiProcessorCount;
     if (const char* sw = std::getenv("FC_SWEEP")) ctx->sweep_tma = std::strcmp(sw, "tma") == 0;
+    {
+        const unsigned hw = std::thread::hardware_concurrency();
+        ctx->copy_threads = (int)std::max(1u, std::min(8u, hw ? hw / 2 : 1u));
+        if (const char* e = std::getenv("FC_COPY_THREADS")) ctx->copy_threads = std::max(1, std::atoi(e));
+    }
     CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CU(cudaMalloc(&ctx->d_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_state, sizeof(DevState)));
@@ -750,20 +890,25 @@ void fc_destroy(fc_ctx* ctx) {
     prof_harvest(ctx);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
-    for (int k = 0; k < 3; ++k) dfree(&ctx->d_U[k]);
-    for (int k = 0; k < 4; ++k) dfree(&ctx->d_xs[k]);
-    for (int k = 0; k < 3; ++k) dfree(&ctx->d_rowterm[k]);
-    for (int k = 0; k < 2; ++k) { dfree(&ctx->d_gpart[k]); dfree(&ctx->d_gfull[k]); }
-    dfree(&ctx->d_prod);
-    dfree(&ctx->d_spart);
-    dfree(&ctx->d_totals);
-    dfree(&ctx->d_chain_in);
-    dfree(&ctx->d_counter);
-    dfree(&ctx->d_state);
-    dfree(&ctx->d_trace);
-    dfree(&ctx->d_row_ptr);
-    dfree(&ctx->d_col);
-    dfree(&ctx->d_val);
+    for (int k = 0; k < 3; ++k) dfree(ctx, &ctx->d_U[k]);
+    for (int k = 0; k < 4; ++k) dfree(ctx, &ctx->d_xs[k]);
+    for (int k = 0; k < 3; ++k) dfree(ctx, &ctx->d_rowterm[k]);
+    for (int k = 0; k < 2; ++k) { dfree(ctx, &ctx->d_gpart[k]); dfree(ctx, &ctx->d_gfull[k]); }
+    dfree(ctx, &ctx->d_prod);
+    dfree(ctx, &ctx->d_spart);
+    dfree(ctx, &ctx->d_totals);
+    dfree(ctx, &ctx->d_chain_in);
+    dfree(ctx, &ctx->d_counter);
+    dfree(ctx, &ctx->d_state);
+    dfree(ctx, &ctx->d_trace);
+    dfree(ctx, &ctx->d_row_ptr);
+    dfree(ctx, &ctx->d_col);
+    dfree(ctx, &ctx->d_val);
+    dfree(ctx, &ctx->d_deg);
+    for (int k = 0; k < fc_ctx::kStageBufs; ++k) {
+        if (ctx->stage_buf[k]) cudaFreeHost(ctx->stage_buf[k]);
+        if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);
+    }
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
     if (ctx->h_done) cudaFreeHost(ctx->h_done);
     for (auto e : ctx->chunk_ev) if (e) cudaEventDestroy(e);
@@ -798,9 +943,10 @@ int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr,
     if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
     CU(cudaSetDevice(ctx->device));
     if (n == 0) return set_err(ctx, FC_INVALID, "membership: empty matrix");
-    if (n > 0xFFFFFFFFULL) return set_err(ctx, FC_INVALID, "similarity: more than 2^32 nodes");
+    if (n >= 0x80000000ULL) return set_err(ctx, FC_INVALID, "similarity: 2^31 or more nodes");
     if (row_ptr[0] != 0 || (uint64_t)row_ptr[n] != nnz)
         return set_err(ctx, FC_INVALID, "similarity: row_ptr does not span [0, nnz)");
+    HostPhase hp_all("upload_csr");
     CU(cudaStreamSynchronize(ctx->stream));
     const int parts = ctx->world > 1 ? ctx->world : ctx->vshards;
     ctx->bounds.assign(parts + 1, 0);
@@ -835,15 +981,34 @@ int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr,
         for (uint64_t k = 0; k < nnz && !weighted; ++k) weighted = values[k] != 1.0;
     }
     if (weighted) TRY(dalloc(ctx, &ctx->d_val, lnnz));
-    else dfree(&ctx->d_val);
+    else dfree(ctx, &ctx->d_val);
     {
         std::vector<long long> rp(lrow + 1);
         for (uint64_t i = 0; i <= lrow; ++i) rp[i] = (long long)(row_ptr[r0 + i] - e0);
-        TRY(h2d(ctx, ctx->d_row_ptr, rp.data(), rp.size() * sizeof(long long)));
+        TRY(h2d_big(ctx, ctx->d_row_ptr, rp.data(), rp.size() * sizeof(long long)));
         CU(cudaStreamSynchronize(ctx->stream));
     }
-    CU(cudaMemcpy(ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    if (weighted) CU(cudaMemcpy(ctx->d_val, values + e0, lnnz * sizeof(double), cudaMemcpyHostToDevice));
+    {
+        HostPhase hp("upload col");
+        TRY(h2d_big(ctx, ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t)));
+    }
+    if (weighted) TRY(h2d_big(ctx, ctx->d_val, values + e0, lnnz * sizeof(double)));
+    // node degrees (== column counts, S symmetric) for the hot-row L2 policy
+    {
+        HostPhase hp("degrees");
+        std::vector<unsigned> deg(n);
+        uint64_t maxd = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            deg[i] = (unsigned)std::min<int64_t>(row_ptr[i + 1] - row_ptr[i], 0xFFFFFFFELL);
+            maxd = std::max<uint64_t>(maxd, deg[i]);
+        }
+        ctx->deg_hist.assign(maxd + 1, 0);
+        for (uint64_t i = 0; i < n; ++i) ctx->deg_hist[deg[i]]++;
+        TRY(dalloc(ctx, &ctx->d_deg, n));
+        CU(cudaMemcpy(ctx->d_deg, deg.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice));
+    }
+    ctx->local_nnz = lnnz;
+    ctx->hot_threshold = 0xFFFFFFFFu;
     ctx->n = n;
     ctx->nnz = nnz;
     ctx->frob_s = frob_sq;
@@ -865,7 +1030,7 @@ int fc_share_matrix(fc_ctx* ctx, uint32_t c, const double* x, double* g_out) {
     if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
     CU(cudaSetDevice(ctx->device));
     TRY(ensure_work(ctx, c, false));
-    TRY(h2d(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
+    TRY(h2d_big(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
     DevState s = base_state(ctx);
     s.sw_b = 0;
     TRY(upload_state(ctx, s));
@@ -895,9 +1060,9 @@ int fc_fused_column_pass(fc_ctx* ctx, uint32_t c, const double* x, double* xs_ou
     if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
     CU(cudaSetDevice(ctx->device));
     TRY(ensure_work(ctx, c, false));
-    TRY(h2d(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
+    TRY(h2d_big(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
     TRY(pass_on_u0(ctx, c, merge_out));
-    if (xs_out) TRY(d2h(ctx, xs_out, ctx->d_xs[0], ctx->n * c * sizeof(double)));
+    if (xs_out) TRY(d2h_big(ctx, xs_out, ctx->d_xs[0], ctx->n * c * sizeof(double)));
     CU(cudaStreamSynchronize(ctx->stream));
     return FC_OK;
 }
@@ -928,7 +1093,7 @@ static int step_from_u0(fc_ctx* ctx, uint32_t c, const double* g, double tau, do
     TRY(upload_state(ctx, s));
     TRY(phase_step(ctx, 0));
     TRY(d2h(ctx, ctx->h_state, ctx->d_state, sizeof(DevState)));
-    TRY(d2h(ctx, x_out, ctx->d_U[1], ctx->n * c * sizeof(double)));
+    TRY(d2h_big(ctx, x_out, ctx->d_U[1], ctx->n * c * sizeof(double)));
     CU(cudaStreamSynchronize(ctx->stream));
     if (ctx->h_state->error) return set_err(ctx, FC_INVALID, "project_simplex: non-finite entry");
     return FC_OK;
@@ -939,8 +1104,8 @@ int fc_gpa_step_fused(fc_ctx* ctx, uint32_t c, const double* x, const double* g,
     if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
     CU(cudaSetDevice(ctx->device));
     TRY(ensure_work(ctx, c, false));
-    TRY(h2d(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
-    TRY(h2d(ctx, ctx->d_xs[0], xs, ctx->n * c * sizeof(double)));
+    TRY(h2d_big(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
+    TRY(h2d_big(ctx, ctx->d_xs[0], xs, ctx->n * c * sizeof(double)));
     return step_from_u0(ctx, c, g, tau, x_out);
 }
 
@@ -948,7 +1113,7 @@ int fc_gpa_step(fc_ctx* ctx, uint32_t c, const double* x, const double* g, doubl
     if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
     CU(cudaSetDevice(ctx->device));
     TRY(ensure_work(ctx, c, false));
-    TRY(h2d(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
+    TRY(h2d_big(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
     TRY(pass_on_u0(ctx, c, nullptr));
     return step_from_u0(ctx, c, g, tau, x_out);
 }
@@ -1031,11 +1196,19 @@ int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const 
         return set_err(ctx, FC_INVALID, "solver: backtracking FISTA needs a single-rank context");
     if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
     if (c == 0) return set_err(ctx, FC_INVALID, "membership: empty matrix");
-    TRY(ensure_work(ctx, c, bt));
-    TRY(ensure_trace(ctx, std::min<uint64_t>(cfg->max_iter + 2, 1u << 20)));
-
-    TRY(h2d(ctx, ctx->d_U[0], x0, ctx->n * c * sizeof(double)));
-    TRY(validate_x(ctx, 0, 1e-9));   // x0.validate(1e-9), solver.hpp:140 / :191
+    {
+        HostPhase hp("ensure_work");
+        TRY(ensure_work(ctx, c, bt));
+        TRY(ensure_trace(ctx, std::min<uint64_t>(cfg->max_iter + 2, 1u << 20)));
+    }
+    {
+        HostPhase hp("x0 h2d");
+        TRY(h2d_big(ctx, ctx->d_U[0], x0, ctx->n * c * sizeof(double)));
+    }
+    {
+        HostPhase hp("validate x0");
+        TRY(validate_x(ctx, 0, 1e-9));   // x0.validate(1e-9), solver.hpp:140 / :191
+    }
 
     // resolve_step_size, solver.hpp:78-85
     const double tau = cfg->step_size > 0.0 ? cfg->step_size
@@ -1103,9 +1276,13 @@ int fc_solver_end(fc_ctx* ctx, double* x_out, fc_trace_record* trace, uint64_t t
     if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
     CU(cudaSetDevice(ctx->device));
     int done = 0;
-    TRY(session_done(ctx, &done));
+    {
+        HostPhase hp("wait device");
+        TRY(session_done(ctx, &done));
+    }
     const DevState& s = *ctx->h_state;
-    if (x_out) TRY(d2h(ctx, x_out, ctx->d_U[s.result_buf], ctx->n * ctx->c * sizeof(double)));
+    HostPhase hp("result d2h");
+    if (x_out) TRY(d2h_big(ctx, x_out, ctx->d_U[s.result_buf], ctx->n * ctx->c * sizeof(double)));
     const uint64_t nrec = std::min<uint64_t>(std::min<uint64_t>(s.n_records, ctx->trace_alloc), trace_cap);
     if (trace && nrec) TRY(d2h(ctx, trace, ctx->d_trace, nrec * sizeof(fc_trace_record)));
     CU(cudaStreamSynchronize(ctx->stream));

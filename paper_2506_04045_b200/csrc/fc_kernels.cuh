@@ -134,6 +134,25 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_normal() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ldg_hint(const double* p, unsigned long long pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// Column indices carry a "hot row" flag in bit 31 (set by k_flag_hot).
+constexpr unsigned kHotBit = 0x80000000u;
+constexpr unsigned kIdxMask = 0x7fffffffu;
+
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __host__ __device__ __forceinline__ unsigned pair_index(unsigned r, unsigned s, unsigned C) {
@@ -334,8 +353,9 @@ __device__ __forceinline__ double group_seq_sum_m(const double (&a)[S], int C, u
 // =============================================================================
 template <int G, int S, bool DUAL, bool W, bool EXACT>
 __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const double* __restrict__ P, double beta,
-                                            unsigned myoff, double myw, int cnt, unsigned gmask, unsigned lg,
-                                            unsigned C, double (&ab)[S], double (&ae)[S]) {
+                                            unsigned myidx, double myw, int cnt, unsigned gmask, unsigned lg,
+                                            unsigned C, double (&ab)[S], double (&ae)[S], unsigned long long pol_hot,
+                                            unsigned long long pol_cold) {
     constexpr int U = (G < 8) ? G : 8;
     if (cnt == G) {
 #pragma unroll
@@ -344,12 +364,14 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
             double vp[DUAL ? U : 1][S];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const unsigned o = __shfl_sync(gmask, myoff, k0 + u, G);
+                const unsigned raw = __shfl_sync(gmask, myidx, k0 + u, G);
+                const unsigned o = (raw & kIdxMask) * C;
+                const unsigned long long pol = (raw & kHotBit) ? pol_hot : pol_cold;
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const bool okc = EXACT || lg + s * G < C;
-                    vb[u][s] = okc ? ldg(B + o + s * G) : 0.0;
-                    if (DUAL) vp[u][s] = okc ? ldg(P + o + s * G) : 0.0;
+                    vb[u][s] = okc ? ldg_hint(B + o + s * G, pol) : 0.0;
+                    if (DUAL) vp[u][s] = okc ? ldg_hint(P + o + s * G, pol) : 0.0;
                 }
             }
 #pragma unroll
@@ -371,13 +393,15 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
             double vp[DUAL ? U : 1][S];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const unsigned o = __shfl_sync(gmask, myoff, k0 + u, G);
+                const unsigned raw = __shfl_sync(gmask, myidx, k0 + u, G);
+                const unsigned o = (raw & kIdxMask) * C;
+                const unsigned long long pol = (raw & kHotBit) ? pol_hot : pol_cold;
                 const bool ok = k0 + u < cnt;
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const bool okc = ok && (EXACT || lg + s * G < C);
-                    vb[u][s] = okc ? ldg(B + o + s * G) : 0.0;
-                    if (DUAL) vp[u][s] = okc ? ldg(P + o + s * G) : 0.0;
+                    vb[u][s] = okc ? ldg_hint(B + o + s * G, pol) : 0.0;
+                    if (DUAL) vp[u][s] = okc ? ldg_hint(P + o + s * G, pol) : 0.0;
                 }
             }
 #pragma unroll
@@ -418,6 +442,8 @@ __global__ void __launch_bounds__(256, 4) k_sweep(Bufs b, Geo g) {
     const double beta = st->beta_next;
     double* xs_main = (DUAL ? b.xs[st->xs_w * 2 + kMatBar] : b.xs[st->xs_w * 2 + kMatExt]) + lg;
     double* xs_ext = b.xs[st->xs_w * 2 + kMatExt] + lg;
+    const unsigned long long pol_hot = l2_policy_evict_last();
+    const unsigned long long pol_cold = l2_policy_evict_normal();
 
     for (;;) {
         unsigned base = 0;
@@ -449,7 +475,7 @@ __global__ void __launch_bounds__(256, 4) k_sweep(Bufs b, Geo g) {
 #pragma unroll
             for (int s = 0; s < S; ++s) { ab[s] = 0.0; ae[s] = 0.0; }
             for (long long eb = e0; eb < e1; eb += G) {
-                const unsigned myoff = nxt_idx * C;
+                const unsigned myidx = nxt_idx;
                 const double myw = nxt_w;
                 const int cnt = (int)min((long long)G, e1 - eb);
                 const long long pn = eb + cnt;               // next chunk: this row or the next one
@@ -457,7 +483,7 @@ __global__ void __launch_bounds__(256, 4) k_sweep(Bufs b, Geo g) {
                     nxt_idx = __ldg(b.col + pn + lg);
                     if (W) nxt_w = ldg(b.val + pn + lg);
                 }
-                sweep_chunk<G, S, DUAL, W, EXACT>(B, P, beta, myoff, myw, cnt, gmask, lg, C, ab, ae);
+                sweep_chunk<G, S, DUAL, W, EXACT>(B, P, beta, myidx, myw, cnt, gmask, lg, C, ab, ae, pol_hot, pol_cold);
             }
             e = e1;
             double a[S];
@@ -590,14 +616,14 @@ __global__ void __launch_bounds__(kSwTmaThreads) k_sweep_tma(Bufs b, Geo g, cons
 
         long long next_issue = 0;
         int idx_pf = 0;                                    // prefetched column index (lane k < Q)
-        if ((long long)lane < (long long)Q && e_lo + lane < e_hi) idx_pf = (int)__ldg(b.col + e_lo + lane);
+        if ((long long)lane < (long long)Q && e_lo + lane < e_hi) idx_pf = (int)(__ldg(b.col + e_lo + lane) & kIdxMask);
         auto issue = [&](long long c) {
             const int sidx = (int)(c % kSwStages);
             const long long p0 = e_lo + c * Q;
             const int cnt = (int)min((long long)Q, e_hi - p0);
             int idx = idx_pf;
             const long long pn = p0 + Q;
-            if ((long long)lane < (long long)Q && pn + lane < e_hi) idx_pf = (int)__ldg(b.col + pn + lane);
+            if ((long long)lane < (long long)Q && pn + lane < e_hi) idx_pf = (int)(__ldg(b.col + pn + lane) & kIdxMask);
             const int last = __shfl_sync(kFull, idx, cnt - 1);
             if ((int)lane >= cnt) idx = last;              // pad a partial gather4 with a valid row
             const int ng = (cnt + 3) >> 2;
@@ -1224,6 +1250,16 @@ __global__ void k_loss_terms_rows(const double* xs, const double* x, double* out
     double acc = 0.0;
     for (int k = 0; k < C; ++k) acc = dadd(acc, dmul(xs[i * C + k], x[i * C + k]));
     out[i] = acc;
+}
+
+// Set / clear the hot-row flag (bit 31) of every stored column index:
+// hot iff deg[j] >= threshold (threshold 0xFFFFFFFF clears all flags).
+__global__ void k_flag_hot(unsigned* col, unsigned long long nnz, const unsigned* deg, unsigned threshold) {
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < nnz;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned j = col[e] & kIdxMask;
+        col[e] = j | (deg[j] >= threshold ? kHotBit : 0u);
+    }
 }
 
 // Device clock origin of TraceRecord::elapsed_ms.
