@@ -123,6 +123,7 @@ struct fc_ctx {
     cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
 
     bool sweep_tma = false;            // FC_SWEEP=tma selects the TMA gather4 sweep
+    bool sweep_groups = false;         // FC_SWEEP=groups: per-group row sweep for C <= 16
     bool umaps_ok = false;
     UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
 
@@ -292,10 +293,30 @@ int launch_sweep_tma(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     return FC_OK;
 }
 
+template <int G, bool DUAL, bool W>
+int launch_sweep_small(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static int grid = 0;
+    if (!grid) grid = grid_for((const void*)k_sweep_small<G, DUAL, W>, 256, 0, ctx->sm_count);
+    const unsigned long long need = (g.nrows + 31) / 32;
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, (need + 7) / 8));
+    k_sweep_small<G, DUAL, W><<<gr, 256, 0, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_sweep_small launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
 template <int G, int S>
 struct LaunchSweep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, bool dual) {
         if (g.nrows == 0) return FC_OK;
+        if constexpr (G <= 8) {   // measured: C=8 9.5 vs 12.2 ms (E8); C=16 keeps the group sweep (B: 1.52 vs 1.78 ms)
+            if (!ctx->sweep_groups) {
+                const bool w = ctx->weighted;
+                if (dual) return w ? launch_sweep_small<G, true, true>(ctx, b, g) : launch_sweep_small<G, true, false>(ctx, b, g);
+                return w ? launch_sweep_small<G, false, true>(ctx, b, g) : launch_sweep_small<G, false, false>(ctx, b, g);
+            }
+        }
         if (G == 32 && g.C > 16 && (g.C % 4) == 0 && !ctx->weighted && ctx->sweep_tma && ctx->umaps_ok) {
             return dual ? launch_sweep_tma<S, true>(ctx, b, g) : launch_sweep_tma<S, false>(ctx, b, g);
         }
@@ -331,10 +352,31 @@ int launch_step_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     return FC_OK;
 }
 
+template <int CP>
+int launch_step_big(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static int grid = 0;
+    const size_t smem = StepBigCfg<CP>::smem();
+    if (!grid) {
+        CU(cudaFuncSetAttribute(k_step_big<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_big<CP>, kStepBigThreads, smem, ctx->sm_count);
+    }
+    constexpr int per_cta = StepBigCfg<CP>::RB * (kStepBigThreads / 32);
+    const unsigned long long need = (g.nrows + per_cta - 1) / per_cta;
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
+    k_step_big<CP><<<gr, kStepBigThreads, smem, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_big launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
 template <int G, int S>
 struct LaunchStep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, int bt) {
         if (g.nrows == 0) return FC_OK;
+        if constexpr (S > 1) {
+            if (!bt) return launch_step_big<32 * S>(ctx, b, g);
+        }
         if (S == 1 && !bt) {   // thread-per-row projection
             return g.C == (unsigned)G ? launch_step_t<G, true>(ctx, b, g) : launch_step_t<G, false>(ctx, b, g);
         }
@@ -838,7 +880,10 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         return set_err(ctx, FC_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a (B200)", device,
                        prop.major, prop.minor);
     ctx->sm_count = prop.multiProcessorCount;
-    if (const char* sw = std::getenv("FC_SWEEP")) ctx->sweep_tma = std::strcmp(sw, "tma") == 0;
+    if (const char* sw = std::getenv("FC_SWEEP")) {
+        ctx->sweep_tma = std::strcmp(sw, "tma") == 0;
+        ctx->sweep_groups = std::strcmp(sw, "groups") == 0;
+    }
     {
         const unsigned hw = std::thread::hardware_concurrency();
         ctx->copy_threads = (int)std::max(1u, std::min(8u, hw ? hw / 2 : 1u));

@@ -713,6 +713,107 @@ __global__ void __launch_bounds__(kSwTmaThreads) k_sweep_tma(Bufs b, Geo g, cons
 }
 
 // =============================================================================
+// K1 for C <= G <= 16: one row per warp at a time; lane = (nonzero slot q,
+// component c) with Q = 32/G slots, so one load instruction gathers Q
+// neighbour rows of the same row i.  The values are then shuffled to the
+// q = 0 lanes in ascending nonzero order and accumulated sequentially there
+// (the reference's order), keeping the warp converged (no per-group row loops).
+// A warp owns a 32-row chunk and walks its rows in order; column indices of the
+// next 32 nonzeros are prefetched.
+// =============================================================================
+template <int G, bool DUAL, bool W>
+__global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
+    const DevState* st = b.st;
+    if (st->done) return;
+    constexpr unsigned kChunk = 32;
+    constexpr int Q = 32 / G;                 // nonzeros per load instruction
+    constexpr int U = (32 / Q) < 8 ? (32 / Q) : 8;  // loads per lane in flight per batch (x2 DUAL)
+    const unsigned C = g.C;
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned c = lane % G, q = lane / G;
+    const bool okc = c < C;
+    const double* __restrict__ B = b.U[st->sw_b] + c;
+    const double* __restrict__ P = DUAL ? b.U[st->sw_p] + c : nullptr;
+    const double beta = st->beta_next;
+    double* xs_main = (DUAL ? b.xs[st->xs_w * 2 + kMatBar] : b.xs[st->xs_w * 2 + kMatExt]) + c;
+    double* xs_ext = b.xs[st->xs_w * 2 + kMatExt] + c;
+
+    for (;;) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(b.counter, kChunk);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= g.nrows) break;
+        const unsigned nr = (unsigned)min((unsigned long long)kChunk, g.nrows - base);
+        const long long myrp = __ldg(b.row_ptr + base + min(lane, nr));
+        const long long e_hi = __ldg(b.row_ptr + base + nr);
+        long long e = __shfl_sync(kFull, myrp, 0);
+        unsigned nxt = 0;
+        double nxtw = 1.0;
+        if (e + lane < e_hi) {
+            nxt = __ldg(b.col + e + lane);
+            if (W) nxtw = ldg(b.val + e + lane);
+        }
+        for (unsigned j = 0; j < nr; ++j) {
+            const long long e0 = e;
+            const long long e1 = (j + 1 < 32u) ? __shfl_sync(kFull, myrp, (j + 1) & 31u) : e_hi;
+            const unsigned long long row = base + j;
+            const double xi = okc ? ldg(B + (size_t)(g.row0 + row) * C) : 0.0;
+            double ab = 0.0, ae = 0.0;
+            for (long long eb = e0; eb < e1; eb += 32) {
+                const unsigned myidx = nxt;
+                const double myw = nxtw;
+                const int cnt = (int)min(32LL, e1 - eb);
+                const long long pn = eb + cnt;
+                if (pn + lane < e_hi) {
+                    nxt = __ldg(b.col + pn + lane);
+                    if (W) nxtw = ldg(b.val + pn + lane);
+                }
+                for (int t0 = 0; t0 < cnt; t0 += Q * U) {
+                    double vb[U], ve[DUAL ? U : 1];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int k = t0 + u * Q + (int)q;           // this lane's nonzero slot
+                        const unsigned raw = __shfl_sync(kFull, myidx, k & 31);
+                        const double w = W ? __shfl_sync(kFull, myw, k & 31) : 1.0;
+                        const bool ok = k < cnt && okc;
+                        const unsigned o = (raw & kIdxMask) * C;
+                        double bv = ok ? ldg(B + o) : 0.0;
+                        if (DUAL) {
+                            const double pv = ok ? ldg(P + o) : 0.0;
+                            const double ev = extrap(bv, pv, beta);
+                            ve[u] = W ? dmul(w, ev) : ev;
+                        }
+                        vb[u] = W ? dmul(w, bv) : bv;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+#pragma unroll
+                        for (int qq = 0; qq < Q; ++qq) {
+                            const int k = t0 + u * Q + qq;
+                            const double bb = __shfl_sync(kFull, vb[u], qq * G + c);
+                            const double ee = DUAL ? __shfl_sync(kFull, ve[u], qq * G + c) : 0.0;
+                            if (k < cnt) {
+                                ab = dadd(ab, bb);
+                                if (DUAL) ae = dadd(ae, ee);
+                            }
+                        }
+                    }
+                }
+            }
+            e = e1;
+            // flush row (q = 0 lanes hold the sums; every lane computed the same chain)
+            if (q == 0 && okc) {
+                xs_main[(size_t)row * C] = ab;
+                if (DUAL) xs_ext[(size_t)row * C] = ae;
+            }
+            const double a1[1] = {dmul(ab, xi)};
+            const double pr = group_seq_sum<G, 1>(a1, (int)C);
+            if (lane == 0) b.prod[row] = pr;
+        }
+    }
+}
+
+// =============================================================================
 // Per-block sequential sums of per-row scalars (objective.hpp:160-170 order):
 //   part[s][blk] = ((0 + v_{1024 blk}) + v_{1024 blk + 1}) + ...
 // One thread per (scalar, block).
@@ -1511,6 +1612,179 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
         for (int p = 0; p < 32; p += RPW) {
             const unsigned long long r2 = rb + p + sub;
             if (r2 < g.nrows && lane_ok) D[(size_t)(g.row0 + r2) * C + lg] = TX[(p + sub) * LD + lg];
+        }
+        __syncwarp();
+    }
+    if (bad) {
+        st->error = 1;
+        st->done = 1;
+    }
+}
+
+// =============================================================================
+// K3 for C in (32, 256] (no backtracking terms): thread-per-row like k_step_t
+// but with the row data in shared memory (CP doubles do not fit registers).
+// Per warp, batches of RB rows:
+//   1 lane-parallel: X_ext rows -> TX (computed in registers), S X_ext rows -> TY (cp.async)
+//   2 thread = row: gradient (4 independent k chains over l ascending; G read
+//     as warp-broadcast double2 from global/L1), y -> TY; projection with a
+//     loop-form bitonic sort of a copy (in TX), the exact threshold test, folds
+//   3 lane-parallel store.
+// CP (64, 128, 256) is the padded width; rows have stride CP+1 (conflict-free).
+// =============================================================================
+template <int CP>
+__device__ void bitonic_desc_smem(double* v) {
+    for (int k = 2; k <= CP; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll 4
+            for (int i = 0; i < CP; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const double a = v[i], b = v[l];
+                    const bool sw = ((i & k) == 0) ? (a < b) : (b < a);
+                    if (sw) {
+                        v[i] = b;
+                        v[l] = a;
+                    }
+                }
+            }
+        }
+    }
+}
+
+constexpr int kStepBigThreads = 64;
+
+template <int CP>
+struct StepBigCfg {
+    static constexpr int RB = CP <= 64 ? 32 : 16;       // rows per warp batch
+    static constexpr int LDB = CP + 1;
+    static size_t smem() { return sizeof(double) * (size_t)(kStepBigThreads / 32) * 2 * RB * LDB; }
+};
+
+template <int CP>
+__global__ void __launch_bounds__(kStepBigThreads) k_step_big(Bufs b, Geo g) {
+    DevState* st = b.st;
+    if (st->done) return;
+    constexpr int RB = StepBigCfg<CP>::RB;
+    constexpr int LDB = StepBigCfg<CP>::LDB;
+    constexpr int S = CP / 32;
+    extern __shared__ double smb[];
+    const int C = (int)g.C;
+    const unsigned lane = threadIdx.x & 31u;
+    const int warp = threadIdx.x >> 5;
+    double* TX = smb + (size_t)warp * 2 * RB * LDB;
+    double* TY = TX + RB * LDB;
+    const int mode = st->step_mode;
+    const double* __restrict__ A = b.U[st->step_a];
+    const double* __restrict__ Bp = b.U[st->step_b];
+    double* __restrict__ D = b.U[st->step_dst];
+    const double beta = st->beta_step;
+    const double tau = st->tau;
+    const int sel = st->step_sel;
+    const double* __restrict__ XS = b.xs[st->xs_r * 2 + sel];
+    const double* __restrict__ Gt = b.gfull[sel];            // Gt[l*C + k] == G[k][l]
+    const bool gvec = (C & 1) == 0;                           // double2 loads of (k, k+1)
+
+    const unsigned long long warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    bool bad = false;
+    for (unsigned long long rb = w0 * RB; rb < g.nrows; rb += warps * RB) {
+        // 1: x rows (registers -> TX), xs rows (cp.async -> TY)
+        for (int p = 0; p < RB; ++p) {
+            const unsigned long long row = rb + p;
+            if (row >= g.nrows) break;
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) {
+                const int r = (int)lane + 32 * s2;
+                if (r < C) {
+                    const size_t a = (size_t)(g.row0 + row) * C + r;
+                    const double av = A[a];
+                    TX[p * LDB + r] = (mode == kLiteral) ? av : extrap(av, Bp[a], beta);
+                    cp_async8(TY + p * LDB + r, XS + (size_t)row * C + r);
+                }
+            }
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        const unsigned long long row = rb + lane;
+        if ((int)lane < RB && row < g.nrows) {
+            double* tx = TX + lane * LDB;
+            double* ty = TY + lane * LDB;
+            // gradient: o_k = sum_l G[k][l] x_l, g_k = -4 (xs_k - o_k) -> ty
+            for (int k0 = 0; k0 < C; k0 += 4) {
+                double o[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int l = 0; l < C; ++l) {
+                    const double xl = tx[l];
+                    const double* gl = Gt + (size_t)l * C + k0;
+                    double gk[4];
+                    if (gvec && k0 + 3 < C) {
+                        const double2 g01 = __ldg(reinterpret_cast<const double2*>(gl));
+                        const double2 g23 = __ldg(reinterpret_cast<const double2*>(gl + 2));
+                        gk[0] = g01.x; gk[1] = g01.y; gk[2] = g23.x; gk[3] = g23.y;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) gk[u] = (k0 + u < C) ? __ldg(gl + u) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) o[u] = dadd(o[u], dmul(gk[u], xl));
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k0 + u < C) ty[k0 + u] = dmul(-4.0, dsub(ty[k0 + u], o[u]));
+            }
+            bool fin = true;
+            for (int k = 0; k < C; ++k) {
+                const double y = dsub(tx[k], dmul(tau, ty[k]));   // solver.hpp:102
+                fin = fin && isfinite(y);
+                ty[k] = y;
+            }
+            if (!fin) {
+                bad = true;
+            } else if (C == 1) {
+                ty[0] = 1.0;
+            } else {
+                // sorted copy in tx (x is dead), -inf padding
+                for (int k = 0; k < CP; ++k) tx[k] = (k < C) ? ty[k] : -INFINITY;
+                bitonic_desc_smem<CP>(tx);
+                double cs = 0.0, a_star = 0.0;
+                int k_star = -1;
+                for (int k = 0; k < C; ++k) {
+                    cs = dadd(cs, tx[k]);
+                    const double a = dsub(cs, 1.0);
+                    if (threshold_cond(tx[k], a, (double)(k + 1))) {
+                        k_star = k;
+                        a_star = a;
+                    }
+                }
+                const double thr = k_star >= 0 ? a_star / (double)(k_star + 1) : 0.0;
+                for (int k = 0; k < C; ++k) ty[k] = ref_max(dsub(ty[k], thr), 0.0);
+                // residual folds (simplex.hpp:43-55), loop form
+                for (int round = 0; round < 4; ++round) {
+                    double sum = 0.0;
+                    for (int k = 0; k < C; ++k) sum = dadd(sum, ty[k]);
+                    const double residual = dsub(sum, 1.0);
+                    if (residual == 0.0) break;
+                    double top = ty[0];
+                    for (int k = 1; k < C; ++k) top = (top < ty[k]) ? ty[k] : top;
+                    int ties = 0;
+                    for (int k = 0; k < C; ++k) ties += (ty[k] == top);
+                    const double share = residual / (double)ties;
+                    for (int k = 0; k < C; ++k)
+                        if (ty[k] == top) ty[k] = ref_max(dsub(ty[k], share), 0.0);
+                }
+            }
+        }
+        __syncwarp();
+        // 3: store bar^n
+        for (int p = 0; p < RB; ++p) {
+            const unsigned long long r2 = rb + p;
+            if (r2 >= g.nrows) break;
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) {
+                const int r = (int)lane + 32 * s2;
+                if (r < C) D[(size_t)(g.row0 + r2) * C + r] = TY[p * LDB + r];
+            }
         }
         __syncwarp();
     }
