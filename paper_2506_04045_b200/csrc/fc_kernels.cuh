@@ -351,12 +351,20 @@ __device__ __forceinline__ double group_seq_sum_m(const double (&a)[S], int C, u
 // take a predicate-free path with U gathers (x2 when DUAL) in flight per lane.
 // EXACT: C == G*S (no idle lanes).
 // =============================================================================
+// Gathers in flight per lane per batch (x2 when DUAL): measured at config C
+// (C=32) 16 -> 36.7 ms vs 8 -> 38.8 ms per sweep; C=16 (config B) prefers 8.
+template <int G>
+struct SweepTune {
+    static constexpr int U = G == 32 ? 16 : (G < 8 ? G : 8);
+    static constexpr int MINB = G == 32 ? 3 : 4;     // CTAs per SM (register budget)
+};
+
 template <int G, int S, bool DUAL, bool W, bool EXACT>
 __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const double* __restrict__ P, double beta,
                                             unsigned myidx, double myw, int cnt, unsigned gmask, unsigned lg,
                                             unsigned C, double (&ab)[S], double (&ae)[S], unsigned long long pol_hot,
                                             unsigned long long pol_cold) {
-    constexpr int U = (G < 8) ? G : 8;
+    constexpr int U = SweepTune<G>::U;
     if (cnt == G) {
 #pragma unroll
         for (int k0 = 0; k0 < G; k0 += U) {
@@ -428,7 +436,7 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
 // prefetches the NEXT chunk's column offsets (same row or the next row) before
 // gathering the current one, so no row waits on its index load.
 template <int G, int S, bool DUAL, bool W, bool EXACT>
-__global__ void __launch_bounds__(256, 4) k_sweep(Bufs b, Geo g) {
+__global__ void __launch_bounds__(256, SweepTune<G>::MINB) k_sweep(Bufs b, Geo g) {
     const DevState* st = b.st;
     if (st->done) return;
     constexpr unsigned kChunk = 32;

@@ -282,3 +282,23 @@ def test_tma_sweep_variant_bitwise(oracle, n, c, monkeypatch):
         assert np.array_equal(xs, xs_o) and m == m_o
     finally:
         t.close()
+
+
+# ---- the NCCL code path on one GPU (1-rank communicator) ------------------------------------
+def test_nccl_path_single_rank_bitwise(oracle, monkeypatch):
+    """FC_FORCE_NCCL=1 runs the multi-GPU schedule (grouped-broadcast allgather,
+    recv -> combine -> send -> broadcast chain) through a real 1-rank NCCL
+    communicator; results must stay bitwise equal to the oracle."""
+    monkeypatch.setenv("FC_FORCE_NCCL", "1")
+    t = capi.Context(0, rank=0, world=1, nccl_id=capi.nccl_unique_id())
+    try:
+        g = random_graph(6000, 7.0, 31)
+        t.upload(g)
+        x0 = oracle.init_random(g.n, 16, 4)
+        for kw in [dict(method=GPA, max_iter=10), dict(method=FISTA, max_iter=10, fista_restart=True),
+                   dict(method=FISTA, max_iter=10, step_size=40 * oracle.default_step_size(g))]:
+            assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+        with pytest.raises(fc.InvalidInput, match="single-rank"):
+            t.share_matrix(x0)
+    finally:
+        t.close()
