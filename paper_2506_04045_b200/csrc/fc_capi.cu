@@ -124,6 +124,7 @@ struct fc_ctx {
 
     bool sweep_tma = false;            // FC_SWEEP=tma selects the TMA gather4 sweep
     bool sweep_groups = false;         // FC_SWEEP=groups: per-group row sweep for C <= 16
+    bool step_big = false;             // FC_STEP=big: thread-per-row k_step_big for C > 32
     bool umaps_ok = false;
     UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
 
@@ -370,12 +371,29 @@ int launch_step_big(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     return FC_OK;
 }
 
+template <int CP>
+int launch_step_wide(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static int grid = 0;
+    const size_t smem = WideCfg<CP>::smem();
+    if (!grid) {
+        CU(cudaFuncSetAttribute(k_step_wide<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_wide<CP>, kWideThreads, smem, ctx->sm_count);
+    }
+    const unsigned long long need = (g.nrows + kWideRows - 1) / kWideRows;
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
+    k_step_wide<CP><<<gr, kWideThreads, smem, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_wide launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
 template <int G, int S>
 struct LaunchStep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, int bt) {
         if (g.nrows == 0) return FC_OK;
         if constexpr (S > 1) {
-            if (!bt) return launch_step_big<32 * S>(ctx, b, g);
+            if (!bt) return ctx->step_big ? launch_step_big<32 * S>(ctx, b, g) : launch_step_wide<32 * S>(ctx, b, g);
         }
         if (S == 1 && !bt) {   // thread-per-row projection
             return g.C == (unsigned)G ? launch_step_t<G, true>(ctx, b, g) : launch_step_t<G, false>(ctx, b, g);
@@ -419,7 +437,7 @@ size_t nchains_of(uint32_t c) { return 2 * (size_t)npairs_of(c) + kNumScal; }
 
 int gram_rows_per_chunk(uint32_t c) {
     const int c4 = (int)((c + 3) & ~3u);
-    return std::max(4, std::min(32, 1024 / c4));
+    return std::max(4, std::min(16, 512 / c4));
 }
 
 // Tensor maps for the TMA gather4 sweep: U[k] as a 2-D [N][C] f64 tensor, box {C, 1}.
@@ -580,8 +598,9 @@ int phase_gram(fc_ctx* ctx, bool dual) {
         const Geo g = make_geo(ctx, s);
         if (g.nblk == 0) continue;
         const Bufs b = make_bufs(ctx, s);
-        dim3 grid((unsigned)g.nblk, (unsigned)((tiles + kGramThreads - 1) / kGramThreads));
-        k_gram<<<grid, kGramThreads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
+        const int threads = std::min(kGramMaxThreads, (tiles + 31) / 32 * 32);
+        dim3 grid((unsigned)g.nblk, (unsigned)((tiles + threads - 1) / threads));
+        k_gram<<<grid, threads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
         TRY(check_launch(ctx, "k_gram"));
     }
     return FC_OK;
@@ -884,6 +903,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         ctx->sweep_tma = std::strcmp(sw, "tma") == 0;
         ctx->sweep_groups = std::strcmp(sw, "groups") == 0;
     }
+    if (const char* sp = std::getenv("FC_STEP")) ctx->step_big = std::strcmp(sp, "big") == 0;
     {
         const unsigned hw = std::thread::hardware_concurrency();
         ctx->copy_threads = (int)std::max(1u, std::min(8u, hw ? hw / 2 : 1u));

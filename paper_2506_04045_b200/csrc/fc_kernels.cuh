@@ -353,10 +353,10 @@ __device__ __forceinline__ double group_seq_sum_m(const double (&a)[S], int C, u
 // =============================================================================
 // Gathers in flight per lane per batch (x2 when DUAL): measured at config C
 // (C=32) 16 -> 36.7 ms vs 8 -> 38.8 ms per sweep; C=16 (config B) prefers 8.
-template <int G>
+template <int G, int S = 1>
 struct SweepTune {
-    static constexpr int U = G == 32 ? 16 : (G < 8 ? G : 8);
-    static constexpr int MINB = G == 32 ? 3 : 4;     // CTAs per SM (register budget)
+    static constexpr int U = G == 32 ? (16 / S > 2 ? 16 / S : 2) : (G < 8 ? G : 8);
+    static constexpr int MINB = G == 32 ? (S == 1 ? 3 : 2) : 4;     // CTAs per SM (register budget)
 };
 
 template <int G, int S, bool DUAL, bool W, bool EXACT>
@@ -364,7 +364,7 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
                                             unsigned myidx, double myw, int cnt, unsigned gmask, unsigned lg,
                                             unsigned C, double (&ab)[S], double (&ae)[S], unsigned long long pol_hot,
                                             unsigned long long pol_cold) {
-    constexpr int U = SweepTune<G>::U;
+    constexpr int U = SweepTune<G, S>::U;
     if (cnt == G) {
 #pragma unroll
         for (int k0 = 0; k0 < G; k0 += U) {
@@ -436,7 +436,7 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
 // prefetches the NEXT chunk's column offsets (same row or the next row) before
 // gathering the current one, so no row waits on its index load.
 template <int G, int S, bool DUAL, bool W, bool EXACT>
-__global__ void __launch_bounds__(256, SweepTune<G>::MINB) k_sweep(Bufs b, Geo g) {
+__global__ void __launch_bounds__(256, SweepTune<G, S>::MINB) k_sweep(Bufs b, Geo g) {
     const DevState* st = b.st;
     if (st->done) return;
     constexpr unsigned kChunk = 32;
@@ -860,7 +860,7 @@ __global__ void __launch_bounds__(128) k_rowsum(Bufs b, Geo g, int nscal, const 
 // (formed as in solver.hpp:261); single: matrix 0 = the swept point.
 // grid = (blocks, tile groups); blockDim = 128.
 // =============================================================================
-constexpr int kGramThreads = 128;
+constexpr int kGramMaxThreads = 256;   // blockDim = min(256, tiles rounded up to a warp)
 
 // Shared memory of k_gram: 2 stages x (bar [+ prev]) x R x C4, + the ext tile (dual).
 __host__ __device__ inline size_t gram_smem(int C, int dual, int R) {
@@ -868,7 +868,7 @@ __host__ __device__ inline size_t gram_smem(int C, int dual, int R) {
     return sizeof(double) * (size_t)R * C4 * (dual ? 5 : 2);
 }
 
-__global__ void __launch_bounds__(kGramThreads) k_gram(Bufs b, Geo g, int dual, int rows_per_chunk) {
+__global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dual, int rows_per_chunk) {
     const DevState* st = b.st;
     if (st->done) return;
     extern __shared__ double smg[];
@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(kGramThreads) k_gram(Bufs b, Geo g, int dual, 
     const int nT = C4 / 4;
     const int tiles_per_mat = nT * (nT + 1) / 2;
     const int nmat = dual ? 2 : 1;
-    const int tile = blockIdx.y * kGramThreads + threadIdx.x;
+    const int tile = blockIdx.y * blockDim.x + threadIdx.x;
     const bool has = tile < tiles_per_mat * nmat;
     const int mat_local = has ? tile / tiles_per_mat : 0;
     int tt = has ? tile % tiles_per_mat : 0;
@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(kGramThreads) k_gram(Bufs b, Geo g, int dual, 
 
     auto issue = [&](int sidx, unsigned long long cr) {
         const int rows = (int)min((unsigned long long)R, r1 - cr);
-        for (int e = threadIdx.x; e < rows * C4; e += kGramThreads) {
+        for (int e = threadIdx.x; e < rows * C4; e += blockDim.x) {
             const int rr = e / C4, cc = e % C4;
             if (cc < C) {
                 const size_t a = (size_t)(g.row0 + cr + rr) * C + cc;
@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(kGramThreads) k_gram(Bufs b, Geo g, int dual, 
         const double* tb = smg + sidx * tsz;
         if (dual) {
             const double* tp = smg + (2 + sidx) * tsz;
-            for (int e = threadIdx.x; e < rows * C4; e += kGramThreads) te[e] = extrap(tb[e], tp[e], beta);
+            for (int e = threadIdx.x; e < rows * C4; e += blockDim.x) te[e] = extrap(tb[e], tp[e], beta);
             __syncthreads();
         }
         if (has) {
@@ -1795,6 +1795,225 @@ __global__ void __launch_bounds__(kStepBigThreads) k_step_big(Bufs b, Geo g) {
             }
         }
         __syncwarp();
+    }
+    if (bad) {
+        st->error = 1;
+        st->done = 1;
+    }
+}
+
+// =============================================================================
+// K3 for C in (32, 256] (no backtracking terms), CTA-cooperative:
+//   batch of 32 rows per CTA (128 threads):
+//   1 X_ext rows -> TX, S X_ext rows -> TY (shared, stride CP+1)
+//   2 gradient as a register-tiled GEMM: thread (row group of 4, k group of
+//     KT = CP/16) accumulates o[r][k] = sum_{l ascending} G[k][l] x_r[l] (each
+//     output one sequential DMUL+DADD chain, the reference's order); G streamed
+//     through shared memory in l-chunks (cp.async, double-buffered, l-major:
+//     Gt[l*C + k] == G[k][l] is already that layout)
+//   3 y = x - tau * (-4 (xs - o)) elementwise
+//   4 projection, 4 lanes per row: bitonic sort of a copy (in TX), sequential
+//     cumsum/threshold by the row's first lane, parallel max / tie counts,
+//     sequential residual sums -- values identical to simplex.hpp:18-59
+//   5 coalesced store of bar^n.
+// =============================================================================
+constexpr int kWideThreads = 128;
+constexpr int kWideRows = 32;
+constexpr int kWideLC = 16;                                  // l-chunk of G per stage
+
+template <int CP>
+struct WideCfg {
+    static constexpr int LD = CP + 1;
+    static constexpr int KT = CP / 16;                       // k per thread
+    static size_t smem() {
+        return sizeof(double) * ((size_t)2 * kWideRows * LD + (size_t)2 * kWideLC * CP);
+    }
+};
+
+template <int CP>
+__global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
+    DevState* st = b.st;
+    if (st->done) return;
+    constexpr int LD = WideCfg<CP>::LD;
+    constexpr int KT = WideCfg<CP>::KT;
+    constexpr int R = kWideRows;
+    extern __shared__ double smw[];
+    double* TX = smw;
+    double* TY = TX + R * LD;
+    double* GS = TY + R * LD;                                // [2][kWideLC][CP]
+    __shared__ double thr_s[R];
+    __shared__ int flag_s[R];
+    const int C = (int)g.C;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int mode = st->step_mode;
+    const double* __restrict__ A = b.U[st->step_a];
+    const double* __restrict__ Bp = b.U[st->step_b];
+    double* __restrict__ D = b.U[st->step_dst];
+    const double beta = st->beta_step;
+    const double tau = st->tau;
+    const int sel = st->step_sel;
+    const double* __restrict__ XS = b.xs[st->xs_r * 2 + sel];
+    const double* __restrict__ Gt = b.gfull[sel];
+    const int rg = tid / 16, kg = tid % 16;                  // GEMM: rows 4rg..4rg+3, k = kg + 16 j
+    const int pr = tid / 4, pq = tid % 4;                    // projection: row pr, quarter pq
+    const unsigned qmask = 0xFu << (lane & ~3);
+    bool bad = false;
+
+    for (unsigned long long rb = (unsigned long long)blockIdx.x * R; rb < g.nrows;
+         rb += (unsigned long long)gridDim.x * R) {
+        const int rows = (int)min((unsigned long long)R, g.nrows - rb);
+        // 1: stage rows
+        for (int e = tid; e < rows * C; e += kWideThreads) {
+            const int r = e / C, k = e % C;
+            const size_t a = (size_t)(g.row0 + rb + r) * C + k;
+            const double av = A[a];
+            TX[r * LD + k] = (mode == kLiteral) ? av : extrap(av, Bp[a], beta);
+            TY[r * LD + k] = XS[(size_t)(rb + r) * C + k];
+        }
+        // 2: GEMM over l-chunks of G
+        auto stage_g = [&](int buf, int l0) {
+            const int nl = min(kWideLC, C - l0);
+            double* dst = GS + (size_t)buf * kWideLC * CP;
+            for (int e = tid; e < nl * C; e += kWideThreads) {
+                const int l = e / C, k = e % C;
+                cp_async8(dst + l * CP + k, Gt + (size_t)(l0 + l) * C + k);
+            }
+            cp_async_commit();
+        };
+        double o[4][KT];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < KT; ++j) o[i][j] = 0.0;
+        stage_g(0, 0);
+        int buf = 0;
+        for (int l0 = 0; l0 < C; l0 += kWideLC, buf ^= 1) {
+            if (l0 + kWideLC < C) {
+                stage_g(buf ^ 1, l0 + kWideLC);
+                cp_async_wait_1();
+            } else {
+                cp_async_wait_all();
+            }
+            __syncthreads();
+            const double* gb = GS + (size_t)buf * kWideLC * CP + kg;
+            const int nl = min(kWideLC, C - l0);
+            for (int l = 0; l < nl; ++l) {
+                double xv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) xv[i] = TX[(4 * rg + i) * LD + l0 + l];
+                double gv[KT];
+#pragma unroll
+                for (int j = 0; j < KT; ++j) gv[j] = gb[l * CP + 16 * j];   // k = kg + 16 j
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < KT; ++j) o[i][j] = dadd(o[i][j], dmul(gv[j], xv[i]));
+            }
+            __syncthreads();
+        }
+        // 3: grad and step (objective.hpp:116-117, solver.hpp:102)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = 4 * rg + i;
+#pragma unroll
+            for (int j = 0; j < KT; ++j) {
+                const int k = kg + 16 * j;
+                if (r < rows && k < C) {
+                    const double grad = dmul(-4.0, dsub(TY[r * LD + k], o[i][j]));
+                    TY[r * LD + k] = dsub(TX[r * LD + k], dmul(tau, grad));
+                }
+            }
+        }
+        __syncthreads();
+        // 4: projection, 4 lanes per row
+        const bool live = pr < rows;
+        double* ty = TY + pr * LD;
+        double* tx = TX + pr * LD;
+        bool fin = true;
+        for (int k = pq; k < C; k += 4)
+            if (live && !isfinite(ty[k])) fin = false;
+        const bool row_fin = __all_sync(qmask, fin);
+        if (live && !row_fin) bad = true;
+        const bool work = live && row_fin && C > 1;
+        for (int k = pq; k < CP; k += 4) tx[k] = (work && k < C) ? ty[k] : -INFINITY;
+        __syncwarp();
+        for (int kk = 2; kk <= CP; kk <<= 1) {
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                for (int i = pq; i < CP; i += 4) {
+                    const int l = i ^ jj;
+                    if (l > i) {
+                        const double a = tx[i], c2 = tx[l];
+                        const bool sw = ((i & kk) == 0) ? (a < c2) : (c2 < a);
+                        if (sw) {
+                            tx[i] = c2;
+                            tx[l] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (pq == 0 && work) {
+            double cs = 0.0, a_star = 0.0;
+            int k_star = -1;
+            for (int k = 0; k < C; ++k) {
+                cs = dadd(cs, tx[k]);
+                const double a = dsub(cs, 1.0);
+                if (threshold_cond(tx[k], a, (double)(k + 1))) {
+                    k_star = k;
+                    a_star = a;
+                }
+            }
+            thr_s[pr] = k_star >= 0 ? a_star / (double)(k_star + 1) : 0.0;
+        }
+        __syncwarp();
+        if (work) {
+            const double thr = thr_s[pr];
+            for (int k = pq; k < C; k += 4) ty[k] = ref_max(dsub(ty[k], thr), 0.0);
+        }
+        __syncwarp();
+        // residual folds: sequential sum by lane pq == 0, max / ties by the 4 lanes
+        for (int round = 0; round < 4; ++round) {
+            if (pq == 0) {
+                double sum = 0.0;
+                if (work)
+                    for (int k = 0; k < C; ++k) sum = dadd(sum, ty[k]);
+                const double residual = dsub(sum, 1.0);
+                thr_s[pr] = residual;
+                flag_s[pr] = work && residual != 0.0;
+            }
+            __syncwarp();
+            const bool go = flag_s[pr] != 0;
+            double top = -INFINITY;
+            if (go)
+                for (int k = pq; k < C; k += 4) top = (top < ty[k]) ? ty[k] : top;
+#pragma unroll
+            for (int o2 = 1; o2 < 4; o2 <<= 1) {
+                const double v = __shfl_xor_sync(qmask, top, o2);
+                top = (top < v) ? v : top;
+            }
+            int ties = 0;
+            if (go)
+                for (int k = pq; k < C; k += 4) ties += (ty[k] == top);
+#pragma unroll
+            for (int o2 = 1; o2 < 4; o2 <<= 1) ties += __shfl_xor_sync(qmask, ties, o2);
+            if (go) {
+                const double share = thr_s[pr] / (double)ties;
+                for (int k = pq; k < C; k += 4)
+                    if (ty[k] == top) ty[k] = ref_max(dsub(ty[k], share), 0.0);
+            }
+            __syncwarp();
+            if (!__any_sync(0xffffffffu, go)) break;
+        }
+        if (live && row_fin && C == 1 && pq == 0) ty[0] = 1.0;
+        __syncthreads();
+        // 5: store bar^n
+        for (int e = tid; e < rows * C; e += kWideThreads) {
+            const int r = e / C, k = e % C;
+            D[(size_t)(g.row0 + rb + r) * C + k] = TY[r * LD + k];
+        }
+        __syncthreads();
     }
     if (bad) {
         st->error = 1;

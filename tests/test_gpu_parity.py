@@ -302,3 +302,13 @@ def test_nccl_path_single_rank_bitwise(oracle, monkeypatch):
             t.share_matrix(x0)
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("n,c", [(900, 40), (700, 200), (600, 256)])
+def test_wide_step_odd_and_max_widths(ctx, oracle, n, c):
+    g = random_graph(n, 9.0, n + c)
+    ctx.upload(g)
+    x0 = oracle.init_random(n, c, 8)
+    tau = oracle.default_step_size(g)
+    for kw in [dict(method=GPA, max_iter=8), dict(method=FISTA, max_iter=8, step_size=50 * tau, fista_restart=True)]:
+        assert_same_run(ctx.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
