@@ -587,7 +587,9 @@ int phase_gram(fc_ctx* ctx, bool dual) {
     const int c4 = (int)((c + 3) & ~3u);
     const int nT = c4 / 4;
     const int tiles = nT * (nT + 1) / 2 * (dual ? 2 : 1);
-    const int R = gram_rows_per_chunk(c);
+    int R = gram_rows_per_chunk(c);
+    // few blocks (small N): occupancy is no concern, larger chunks mean fewer barriers
+    if (ctx->local_blocks < (uint64_t)ctx->sm_count * 2) R = std::max(R, std::min(128, 4096 / (int)((c + 3) & ~3u)));
     const size_t smem = gram_smem((int)c, dual ? 1 : 0, R);
     static size_t smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
@@ -625,7 +627,7 @@ int phase_rowsum(fc_ctx* ctx, int bt) {
         if (g.nblk == 0) continue;
         const Bufs b = make_bufs(ctx, s);
         const unsigned long long total = g.nblk * (unsigned long long)nscal;
-        k_rowsum<<<(unsigned)((total + 127) / 128), 128, 0, ctx->stream>>>(
+        k_rowsum<<<(unsigned)total, kRowsumThreads, 0, ctx->stream>>>(
             b, g, nscal, b.prod, bt ? b.rowterm[0] : nullptr, bt ? b.rowterm[1] : nullptr,
             bt ? b.rowterm[2] : nullptr, kScalMerge);
         TRY(check_launch(ctx, "k_rowsum"));

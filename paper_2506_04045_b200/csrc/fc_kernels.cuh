@@ -824,30 +824,33 @@ __global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
 // =============================================================================
 // Per-block sequential sums of per-row scalars (objective.hpp:160-170 order):
 //   part[s][blk] = ((0 + v_{1024 blk}) + v_{1024 blk + 1}) + ...
-// One thread per (scalar, block).
+// One CTA per (scalar, block): the block's values are staged into shared
+// memory by all threads (coalesced), then one thread adds them in order.
 // =============================================================================
-__global__ void __launch_bounds__(128) k_rowsum(Bufs b, Geo g, int nscal, const double* a0,
-                                                const double* a1, const double* a2, const double* a3,
-                                                int slot0) {
+constexpr int kRowsumThreads = 128;
+
+__global__ void __launch_bounds__(kRowsumThreads) k_rowsum(Bufs b, Geo g, int nscal, const double* a0,
+                                                           const double* a1, const double* a2, const double* a3,
+                                                           int slot0) {
     if (b.st->done) return;
-    const unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
-    if (t >= g.nblk * (unsigned long long)nscal) return;
-    const int which = (int)(t / g.nblk);
-    const unsigned long long blk = t % g.nblk;
+    __shared__ double v[kBlock];
+    const int which = (int)(blockIdx.x / g.nblk);
+    const unsigned long long blk = blockIdx.x % g.nblk;
     const double* a = which == 0 ? a0 : which == 1 ? a1 : which == 2 ? a2 : a3;
     const unsigned long long r0 = blk * kBlock;
-    const unsigned long long r1 = min(r0 + kBlock, g.nrows);
-    double m = 0.0;
-    unsigned long long i = r0;
-    for (; i + 8 <= r1; i += 8) {
-        double v[8];
+    const int n = (int)(min(r0 + kBlock, g.nrows) - r0);
+    for (int k = threadIdx.x; k < n; k += kRowsumThreads) v[k] = a[r0 + k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        int k = 0;
+        for (; k + 8 <= n; k += 8) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = a[i + u];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) m = dadd(m, v[u]);
+            for (int u = 0; u < 8; ++u) m = dadd(m, v[k + u]);
+        }
+        for (; k < n; ++k) m = dadd(m, v[k]);
+        b.spart[(size_t)(slot0 + which) * g.spart_stride + blk] = m;
     }
-    for (; i < r1; ++i) m = dadd(m, a[i]);
-    b.spart[(size_t)(slot0 + which) * g.spart_stride + blk] = m;
 }
 
 // =============================================================================
