@@ -100,6 +100,21 @@ void fc_destroy(fc_ctx* ctx);
  * frob_sq is SparseSimilarity::frob_sq() (sum of v*v in stored order). */
 int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr,
                   const uint32_t* col_idx, const double* values, double frob_sq);
+/* SparseSimilarity::from_triplets (sparse.hpp:28-62) on the device: triplets
+ * (row i, column j, value; values NULL = all 1.0) are validated, sorted by
+ * (column, row), checked for duplicates and exact symmetry (the reference's
+ * messages, first failing entry in its loop order), and the CSR is written to
+ * row_ptr_out[n+1] / col_idx_out[nnz] / values_out[nnz] (may be NULL) with
+ * frob_sq and whether every value is 1.0.  The result becomes the context's
+ * resident similarity (as fc_upload_csr: a multi-rank context keeps its shard). */
+int fc_build_from_triplets(fc_ctx* ctx, uint64_t n, uint64_t nnz, const uint32_t* rows, const uint32_t* cols,
+                           const double* values, int64_t* row_ptr_out, uint32_t* col_idx_out, double* values_out,
+                           double* frob_sq_out, int* pattern_only_out);
+/* SparseSimilarity::build_similarity (sparse.hpp:66-75) on the device: A + I
+ * from `num_edges` (u, v) pairs (a normalised Graph's edge list); nnz =
+ * num_nodes + 2 num_edges, all values 1.0. */
+int fc_build_similarity(fc_ctx* ctx, uint64_t num_nodes, uint64_t num_edges, const uint32_t* edges,
+                        int64_t* row_ptr_out, uint32_t* col_idx_out, double* frob_sq_out);
 /* Row bounds of every shard after fc_upload_csr: bounds[0..world]. */
 int fc_partition(const fc_ctx* ctx, uint64_t* bounds, int max_world);
 

@@ -151,6 +151,35 @@ def _ctx_nograph(ctx):
     return ctx or default_context()
 
 
+# ---- sparse.hpp construction on the device (fc_build.cu) ---------------------------
+def _as_u32_index(a) -> np.ndarray:
+    a = np.asarray(a)
+    if a.dtype == np.uint32:
+        return np.ascontiguousarray(a)
+    if a.dtype.kind in "iu" and (a.size == 0 or (int(a.min()) >= 0 and int(a.max()) <= 0xFFFFFFFF)):
+        return a.astype(np.uint32)
+    if a.dtype.kind == "f":
+        a = np.where(np.isfinite(a), a, -1.0)
+    a = a.astype(np.int64)
+    # negative / >= 2^32 ids are out of range for any n < 2^31: map them to 0xFFFFFFFF so the
+    # device check reports the first failing triplet in the reference's order.
+    return np.where((a < 0) | (a > 0xFFFFFFFF), 0xFFFFFFFF, a).astype(np.uint32)
+
+
+def from_triplets(n: int, triplets, ctx: capi.Context | None = None) -> SparseSimilarity:
+    """SparseSimilarity::from_triplets (sparse.hpp:28-62) on the device; the result stays resident."""
+    t = np.asarray(triplets, dtype=np.float64).reshape(-1, 3) if len(triplets) else np.zeros((0, 3))
+    ctx = ctx or default_context()
+    return ctx.build_from_triplets(n, _as_u32_index(t[:, 0]), _as_u32_index(t[:, 1]), t[:, 2])
+
+
+def build_similarity(num_nodes: int, edges, ctx: capi.Context | None = None) -> SparseSimilarity:
+    """SparseSimilarity::build_similarity (sparse.hpp:66-75) on the device; the result stays resident."""
+    e = np.asarray(edges).reshape(-1, 2)
+    ctx = ctx or default_context()
+    return ctx.build_similarity(num_nodes, _as_u32_index(e))
+
+
 # ---- rng.hpp / membership.hpp ------------------------------------------------------
 _GOLDEN = np.uint64(0x9E3779B97F4A7C15)
 

@@ -77,6 +77,9 @@ SIGNATURES = {
     "fc_kernel_times": (C.c_int, [C.c_void_p, _dp, _u64p, C.c_int]),
     "fc_plan_partition": (C.c_int, [C.c_uint64, _i64p, C.c_int, _u64p]),
     "fc_generate_graph": (C.c_int, [C.POINTER(GraphSpecC), _u64p, C.POINTER(_i64p), C.POINTER(_u32p)]),
+    "fc_build_from_triplets": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _u32p, _u32p, _dp, _i64p, _u32p, _dp,
+                                         _dp, C.POINTER(C.c_int)]),
+    "fc_build_similarity": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _u32p, _i64p, _u32p, _dp]),
     "fc_free": (None, [C.c_void_p]),
 }
 
@@ -181,6 +184,45 @@ class Context:
     def upload(self, graph) -> None:
         self._c(lib().fc_upload_csr(self.h, graph.n, graph.nnz, _p(graph.row_ptr, _i64p),
                                     _p(graph.col_idx, _u32p), _p(graph.values), graph.frob_sq))
+        self.n = graph.n
+        try:
+            self._graph_ref = weakref.ref(graph)
+        except TypeError:
+            self._graph_ref = None
+
+    def build_from_triplets(self, n, rows, cols, values=None):
+        """fc_build_from_triplets: device from_triplets; the result is resident and returned."""
+        from .similarity import SparseSimilarity
+        rows = np.ascontiguousarray(rows, dtype=np.uint32)
+        cols = np.ascontiguousarray(cols, dtype=np.uint32)
+        nnz = rows.size
+        vals = None if values is None else np.ascontiguousarray(values, dtype=np.float64)
+        rp = np.empty(int(n) + 1, np.int64)
+        ci = np.empty(nnz, np.uint32)
+        vo = np.empty(nnz, np.float64) if vals is not None else None
+        frob = C.c_double()
+        pat = C.c_int()
+        self._c(lib().fc_build_from_triplets(self.h, int(n), nnz, _p(rows, _u32p), _p(cols, _u32p), _p(vals),
+                                             _p(rp, _i64p), _p(ci, _u32p), _p(vo), C.byref(frob), C.byref(pat)))
+        s = SparseSimilarity(int(n), rp, ci, None if pat.value else vo, frob.value)
+        self._adopt(s)
+        return s
+
+    def build_similarity(self, num_nodes, edges):
+        """fc_build_similarity: device A + I from an (m, 2) edge list; resident and returned."""
+        from .similarity import SparseSimilarity
+        e = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+        nnz = int(num_nodes) + 2 * e.shape[0]
+        rp = np.empty(int(num_nodes) + 1, np.int64)
+        ci = np.empty(nnz, np.uint32)
+        frob = C.c_double()
+        self._c(lib().fc_build_similarity(self.h, int(num_nodes), e.shape[0], _p(e, _u32p), _p(rp, _i64p),
+                                          _p(ci, _u32p), C.byref(frob)))
+        s = SparseSimilarity(int(num_nodes), rp, ci, None, frob.value)
+        self._adopt(s)
+        return s
+
+    def _adopt(self, graph):
         self.n = graph.n
         try:
             self._graph_ref = weakref.ref(graph)

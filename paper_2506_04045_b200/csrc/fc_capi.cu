@@ -33,6 +33,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "fc_internal.h"
 #include "fc_kernels.cuh"
 #include "fuzzyclust_cuda.h"
 
@@ -861,6 +862,20 @@ bool granular_ok(fc_ctx* ctx) { return ctx->comm == nullptr; }
 
 }  // namespace
 
+cudaStream_t fc_internal_stream(fc_ctx* ctx) { return ctx->stream; }
+int fc_internal_device(fc_ctx* ctx) { return ctx->device; }
+int fc_internal_fail(fc_ctx* ctx, int code, const std::string& msg) { return set_err(ctx, code, "%s", msg.c_str()); }
+extern "C" {
+static int upload_csr_impl(fc_ctx*, uint64_t, uint64_t, const int64_t*, const uint32_t*, const double*, double, bool,
+                           int);
+}
+int fc_internal_h2d(fc_ctx* ctx, void* dst, const void* src, size_t bytes) { return h2d_big(ctx, dst, src, bytes); }
+int fc_internal_d2h(fc_ctx* ctx, void* dst, const void* src, size_t bytes) { return d2h_big(ctx, dst, src, bytes); }
+int fc_internal_adopt_device_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* h_row_ptr,
+                                 const uint32_t* d_col, const double* d_val, double frob_sq) {
+    return upload_csr_impl(ctx, n, nnz, h_row_ptr, d_col, d_val, frob_sq, true, d_val ? 1 : 0);
+}
+
 // =====================================================================================
 extern "C" {
 
@@ -1008,8 +1023,11 @@ int fc_plan_partition(uint64_t n, const int64_t* row_ptr, int world, uint64_t* b
     return FC_OK;
 }
 
-int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr, const uint32_t* col_idx,
-                  const double* values, double frob_sq) {
+// fc_upload_csr's body.  row_ptr is a host array; col_idx / values are host arrays, or
+// device arrays of the whole matrix when src_device (fc_build.cu adopting what it
+// built: the shard slice is copied device to device).  weighted_hint: -1 = scan values.
+static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr, const uint32_t* col_idx,
+                           const double* values, double frob_sq, bool src_device, int weighted_hint) {
     if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
     CU(cudaSetDevice(ctx->device));
     if (n == 0) return set_err(ctx, FC_INVALID, "membership: empty matrix");
@@ -1046,8 +1064,8 @@ int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr,
     const uint64_t lnnz = (uint64_t)(e1 - e0);
     TRY(dalloc(ctx, &ctx->d_row_ptr, lrow + 1));
     TRY(dalloc(ctx, &ctx->d_col, lnnz));
-    bool weighted = false;
-    if (values) {
+    bool weighted = weighted_hint > 0;
+    if (values && weighted_hint < 0) {
         for (uint64_t k = 0; k < nnz && !weighted; ++k) weighted = values[k] != 1.0;
     }
     if (weighted) TRY(dalloc(ctx, &ctx->d_val, lnnz));
@@ -1058,11 +1076,18 @@ int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr,
         TRY(h2d_big(ctx, ctx->d_row_ptr, rp.data(), rp.size() * sizeof(long long)));
         CU(cudaStreamSynchronize(ctx->stream));
     }
-    {
-        HostPhase hp("upload col");
-        TRY(h2d_big(ctx, ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t)));
+    if (src_device) {
+        CU(cudaMemcpyAsync(ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        if (weighted)
+            CU(cudaMemcpyAsync(ctx->d_val, values + e0, lnnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    } else {
+        {
+            HostPhase hp("upload col");
+            TRY(h2d_big(ctx, ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t)));
+        }
+        if (weighted) TRY(h2d_big(ctx, ctx->d_val, values + e0, lnnz * sizeof(double)));
     }
-    if (weighted) TRY(h2d_big(ctx, ctx->d_val, values + e0, lnnz * sizeof(double)));
     // node degrees (== column counts, S symmetric) for the hot-row L2 policy
     {
         HostPhase hp("degrees");
@@ -1086,6 +1111,11 @@ int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr,
     ctx->have_csr = true;
     ctx->c = 0;   // force buffer re-allocation for the new N
     return FC_OK;
+}
+
+int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr, const uint32_t* col_idx,
+                  const double* values, double frob_sq) {
+    return upload_csr_impl(ctx, n, nnz, row_ptr, col_idx, values, frob_sq, false, -1);
 }
 
 int fc_partition(const fc_ctx* ctx, uint64_t* bounds, int max_world) {

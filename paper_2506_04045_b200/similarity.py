@@ -69,10 +69,13 @@ class SparseSimilarity:
         i = t[:, 0].astype(np.int64)
         j = t[:, 1].astype(np.int64)
         v = t[:, 2]
-        if np.any((i < 0) | (j < 0) | (i >= n) | (j >= n)):
-            raise InvalidInput("similarity: index out of range")
-        if np.any(~np.isfinite(v)) or np.any(v < 0.0):
-            raise InvalidInput("similarity: values must be finite and nonnegative")
+        # per triplet, range before value (sparse.hpp:30-33): the first failing triplet decides
+        bad_r = (i < 0) | (j < 0) | (i >= n) | (j >= n)
+        bad = bad_r | ~np.isfinite(v) | (v < 0.0)
+        if bad.any():
+            k = int(np.argmax(bad))
+            raise InvalidInput("similarity: index out of range" if bad_r[k]
+                               else "similarity: values must be finite and nonnegative")
         order = np.lexsort((i, j))
         i, j, v = i[order], j[order], v[order]
         if i.size > 1 and np.any((i[1:] == i[:-1]) & (j[1:] == j[:-1])):
