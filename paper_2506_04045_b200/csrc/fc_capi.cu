@@ -108,7 +108,10 @@ struct fc_ctx {
     double* d_totals = nullptr;        // (vshards + 1) slots
     double* d_chain_in = nullptr;
     double* d_gfull[2] = {nullptr, nullptr};
-    unsigned* d_counter = nullptr;
+    unsigned* d_counter = nullptr;    // [0, 64): row-chunk schedulers per shard; [64, 128): heavy-row schedulers
+    unsigned* d_heavy = nullptr;      // per shard: local rows of degree >= heavy_deg, by degree descending
+    std::vector<uint64_t> heavy_off, heavy_cnt;
+    unsigned heavy_deg = 1024;
     DevState* d_state = nullptr;
     DevState* h_state = nullptr;       // pinned mirror
     int* h_done = nullptr;             // pinned, 2 slots
@@ -124,7 +127,7 @@ struct fc_ctx {
     cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
 
     bool sweep_tma = false;            // FC_SWEEP=tma selects the TMA gather4 sweep
-    bool sweep_groups = false;         // FC_SWEEP=groups: per-group row sweep for C <= 16
+    bool sweep_groups = false;       // FC_SWEEP=groups: per-group row sweep for C <= 16
     bool step_big = false;             // FC_STEP=big: thread-per-row k_step_big for C > 32
     bool umaps_ok = false;
     UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
@@ -548,6 +551,10 @@ Bufs make_bufs(fc_ctx* ctx, size_t s) {
     b.trace = ctx->d_trace;
     b.st = ctx->d_state;
     b.counter = ctx->d_counter + s;
+    b.hcounter = ctx->d_counter + 64 + s;
+    b.heavy = ctx->d_heavy ? ctx->d_heavy + ctx->heavy_off[s] : nullptr;
+    b.nheavy = ctx->d_heavy ? (unsigned)ctx->heavy_cnt[s] : 0u;
+    b.heavy_deg = ctx->heavy_deg;
     return b;
 }
 
@@ -612,6 +619,7 @@ int phase_gram(fc_ctx* ctx, bool dual) {
 int phase_sweep(fc_ctx* ctx, bool dual) {
     ProfScope p(ctx, kClsSweep);
     CU(cudaMemsetAsync(ctx->d_counter, 0, ctx->shards.size() * sizeof(unsigned), ctx->stream));
+    CU(cudaMemsetAsync(ctx->d_counter + 64, 0, ctx->shards.size() * sizeof(unsigned), ctx->stream));
     for (size_t s = 0; s < ctx->shards.size(); ++s) {
         const Bufs b = make_bufs(ctx, s);
         const Geo g = make_geo(ctx, s);
@@ -930,7 +938,8 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
     CU(cudaMalloc(&ctx->d_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_done, 2 * sizeof(int)));
-    CU(cudaMalloc(&ctx->d_counter, 64 * sizeof(unsigned)));
+    CU(cudaMalloc(&ctx->d_counter, 128 * sizeof(unsigned)));
+    if (const char* h = std::getenv("FC_HEAVY_DEG")) ctx->heavy_deg = (unsigned)std::max(1L, std::atol(h));
     CU(cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ctx->chunk_ev[1], cudaEventDisableTiming));
     // FC_FORCE_NCCL=1 with world == 1 and an id: a 1-rank communicator, so the
@@ -990,6 +999,7 @@ void fc_destroy(fc_ctx* ctx) {
     dfree(ctx, &ctx->d_col);
     dfree(ctx, &ctx->d_val);
     dfree(ctx, &ctx->d_deg);
+    dfree(ctx, &ctx->d_heavy);
     for (int k = 0; k < fc_ctx::kStageBufs; ++k) {
         if (ctx->stage_buf[k]) cudaFreeHost(ctx->stage_buf[k]);
         if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);
@@ -1101,6 +1111,26 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
         for (uint64_t i = 0; i < n; ++i) ctx->deg_hist[deg[i]]++;
         TRY(dalloc(ctx, &ctx->d_deg, n));
         CU(cudaMemcpy(ctx->d_deg, deg.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice));
+        // heavy rows per shard (k_sweep phase 1), longest first
+        std::vector<unsigned> heavy;
+        ctx->heavy_off.assign(ctx->shards.size(), 0);
+        ctx->heavy_cnt.assign(ctx->shards.size(), 0);
+        for (size_t sh = 0; sh < ctx->shards.size(); ++sh) {
+            const Shard& S = ctx->shards[sh];
+            const size_t first = heavy.size();
+            for (uint64_t i = S.row0; i < S.row0 + S.nrows; ++i)
+                if (deg[i] >= ctx->heavy_deg) heavy.push_back((unsigned)(i - S.row0));
+            std::stable_sort(heavy.begin() + first, heavy.end(),
+                             [&](unsigned a, unsigned b2) { return deg[S.row0 + a] > deg[S.row0 + b2]; });
+            ctx->heavy_off[sh] = first;
+            ctx->heavy_cnt[sh] = heavy.size() - first;
+        }
+        if (heavy.empty()) {
+            dfree(ctx, &ctx->d_heavy);
+        } else {
+            TRY(dalloc(ctx, &ctx->d_heavy, heavy.size()));
+            CU(cudaMemcpy(ctx->d_heavy, heavy.data(), heavy.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
+        }
     }
     ctx->local_nnz = lnnz;
     ctx->hot_threshold = 0xFFFFFFFFu;

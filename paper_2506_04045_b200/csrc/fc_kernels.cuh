@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <cuda.h>
+#include <climits>
 #include <cuda_runtime.h>
 
 namespace fc {
@@ -104,6 +105,10 @@ struct Bufs {
     TraceRec* trace;
     DevState* st;
     unsigned* counter;              // dynamic row scheduler of k_sweep
+    const unsigned* heavy;          // shard-local rows of degree >= heavy_deg, by degree descending
+    unsigned nheavy;
+    unsigned heavy_deg;
+    unsigned* hcounter;             // scheduler of the heavy rows
 };
 
 struct Geo {
@@ -435,6 +440,10 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
 // stretch of the CSR.  The group walks that stretch in G-wide index chunks and
 // prefetches the NEXT chunk's column offsets (same row or the next row) before
 // gathering the current one, so no row waits on its index load.
+// Heavy rows (G == 32, degree >= b.heavy_deg; b.heavy lists them by degree,
+// descending) are handed out FIRST, one per warp, and skipped by the strips:
+// a power-law hub (114k entries at config C) is one sequential chain per
+// component, and started late it would set the kernel's tail.
 template <int G, int S, bool DUAL, bool W, bool EXACT>
 __global__ void __launch_bounds__(256, SweepTune<G, S>::MINB) k_sweep(Bufs b, Geo g) {
     const DevState* st = b.st;
@@ -452,29 +461,40 @@ __global__ void __launch_bounds__(256, SweepTune<G, S>::MINB) k_sweep(Bufs b, Ge
     double* xs_ext = b.xs[st->xs_w * 2 + kMatExt] + lg;
     const unsigned long long pol_hot = l2_policy_evict_last();
     const unsigned long long pol_cold = l2_policy_evict_normal();
+    constexpr bool kHeavy = G == 32;                         // heavy-row phase: full-warp groups only
+    const long long heavy_deg = (kHeavy && b.nheavy) ? (long long)b.heavy_deg : LLONG_MAX;
 
-    for (;;) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(b.counter, kChunk);
-        base = __shfl_sync(kFull, base, 0);
-        if (base >= g.nrows) break;
-        const unsigned nr = (unsigned)min((unsigned long long)kChunk, g.nrows - base);
-        const unsigned r_lo = sub * G;                       // this group's strip [r_lo, r_hi)
-        if (r_lo >= nr) continue;                            // group-divergent from here on
-        const unsigned nrow = min((unsigned)G, nr - r_lo);
-        const long long myrp = __ldg(b.row_ptr + base + r_lo + min(lg, nrow));
-        const long long e_hi = __ldg(b.row_ptr + base + r_lo + nrow);
+    // rows [rb, rb + nrow) of the shard; rows of degree >= tdeg are skipped
+    auto strip = [&](unsigned long long rb, unsigned nrow, long long tdeg) {
+        const long long myrp = __ldg(b.row_ptr + rb + min(lg, nrow));
+        const long long e_hi = __ldg(b.row_ptr + rb + nrow);
+        unsigned skip = 0;
+        if (kHeavy && tdeg != LLONG_MAX) {
+            const long long nb = __shfl_down_sync(gmask, myrp, 1, G);
+            const long long d = ((lg + 1 < (unsigned)G) ? nb : e_hi) - myrp;
+            skip = (__ballot_sync(gmask, lg < nrow && d >= tdeg) >> (sub * G)) & (G == 32 ? kFull : ((1u << G) - 1u));
+        }
         long long e = __shfl_sync(gmask, myrp, 0, G);
         unsigned nxt_idx = 0;                                // raw index: multiplied at use, so the
         double nxt_w = 1.0;                                  // prefetch never waits on its load
-        if (e + lg < e_hi) {
-            nxt_idx = __ldg(b.col + e + lg);
-            if (W) nxt_w = ldg(b.val + e + lg);
-        }
+        bool stale = true;
         for (unsigned j = 0; j < nrow; ++j) {
             const long long e0 = e;
             const long long e1 = (j + 1 < (unsigned)G) ? __shfl_sync(gmask, myrp, j + 1, G) : e_hi;
-            const unsigned long long row = base + r_lo + j;
+            if (kHeavy && ((skip >> j) & 1u)) {              // heavy row: done in the first phase
+                e = e1;
+                stale = true;
+                continue;
+            }
+            if (stale) {
+                nxt_idx = 0;
+                if (e0 + lg < e_hi) {
+                    nxt_idx = __ldg(b.col + e0 + lg);
+                    if (W) nxt_w = ldg(b.val + e0 + lg);
+                }
+                stale = false;
+            }
+            const unsigned long long row = rb + j;
             const size_t own = (size_t)(g.row0 + row) * C;
             double xi[S];
 #pragma unroll
@@ -506,6 +526,39 @@ __global__ void __launch_bounds__(256, SweepTune<G, S>::MINB) k_sweep(Bufs b, Ge
             const double pr = group_seq_sum_m<G, S>(a, (int)C, gmask);
             if (lg == 0) b.prod[row] = pr;
         }
+    };
+
+    // one call site (a second inlined copy of strip() costs registers): heavy rows
+    // first, longest first, then the 32-row chunks
+    bool heavy_phase = kHeavy && heavy_deg != LLONG_MAX;
+    for (;;) {
+        unsigned long long rb;
+        unsigned nrow;
+        long long tdeg;
+        if (heavy_phase) {
+            unsigned h = 0;
+            if (lane == 0) h = atomicAdd(b.hcounter, 1u);
+            h = __shfl_sync(kFull, h, 0);
+            if (h >= b.nheavy) {
+                heavy_phase = false;
+                continue;
+            }
+            rb = b.heavy[h];
+            nrow = 1;
+            tdeg = LLONG_MAX;
+        } else {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(b.counter, kChunk);
+            base = __shfl_sync(kFull, base, 0);
+            if (base >= g.nrows) break;
+            const unsigned nr = (unsigned)min((unsigned long long)kChunk, g.nrows - base);
+            const unsigned r_lo = sub * G;                   // this group's strip [r_lo, r_hi)
+            if (r_lo >= nr) continue;                        // group-divergent from here on
+            rb = base + r_lo;
+            nrow = min((unsigned)G, nr - r_lo);
+            tdeg = heavy_deg;
+        }
+        strip(rb, nrow, tdeg);
     }
 }
 
@@ -746,24 +799,37 @@ __global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
     double* xs_main = (DUAL ? b.xs[st->xs_w * 2 + kMatBar] : b.xs[st->xs_w * 2 + kMatExt]) + c;
     double* xs_ext = b.xs[st->xs_w * 2 + kMatExt] + c;
 
-    for (;;) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(b.counter, kChunk);
-        base = __shfl_sync(kFull, base, 0);
-        if (base >= g.nrows) break;
-        const unsigned nr = (unsigned)min((unsigned long long)kChunk, g.nrows - base);
+    const long long heavy_deg = b.nheavy ? (long long)b.heavy_deg : LLONG_MAX;
+    // rows [base, base + nr); rows of degree >= tdeg were done in the heavy phase
+    auto strip = [&](unsigned long long base, unsigned nr, long long tdeg) {
         const long long myrp = __ldg(b.row_ptr + base + min(lane, nr));
         const long long e_hi = __ldg(b.row_ptr + base + nr);
+        unsigned skip = 0;
+        if (tdeg != LLONG_MAX) {
+            const long long nb = __shfl_down_sync(kFull, myrp, 1);
+            const long long d = ((lane + 1 < 32u) ? nb : e_hi) - myrp;
+            skip = __ballot_sync(kFull, lane < nr && d >= tdeg);
+        }
         long long e = __shfl_sync(kFull, myrp, 0);
         unsigned nxt = 0;
         double nxtw = 1.0;
-        if (e + lane < e_hi) {
-            nxt = __ldg(b.col + e + lane);
-            if (W) nxtw = ldg(b.val + e + lane);
-        }
+        bool stale = true;
         for (unsigned j = 0; j < nr; ++j) {
             const long long e0 = e;
             const long long e1 = (j + 1 < 32u) ? __shfl_sync(kFull, myrp, (j + 1) & 31u) : e_hi;
+            if ((skip >> j) & 1u) {
+                e = e1;
+                stale = true;
+                continue;
+            }
+            if (stale) {
+                nxt = 0;
+                if (e0 + lane < e_hi) {
+                    nxt = __ldg(b.col + e0 + lane);
+                    if (W) nxtw = ldg(b.val + e0 + lane);
+                }
+                stale = false;
+            }
             const unsigned long long row = base + j;
             const double xi = okc ? ldg(B + (size_t)(g.row0 + row) * C) : 0.0;
             double ab = 0.0, ae = 0.0;
@@ -818,6 +884,33 @@ __global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
             const double pr = group_seq_sum<G, 1>(a1, (int)C);
             if (lane == 0) b.prod[row] = pr;
         }
+    };
+    bool heavy_phase = heavy_deg != LLONG_MAX;              // heavy rows first, longest first
+    for (;;) {
+        unsigned long long rb;
+        unsigned nrow;
+        long long tdeg;
+        if (heavy_phase) {
+            unsigned h = 0;
+            if (lane == 0) h = atomicAdd(b.hcounter, 1u);
+            h = __shfl_sync(kFull, h, 0);
+            if (h >= b.nheavy) {
+                heavy_phase = false;
+                continue;
+            }
+            rb = b.heavy[h];
+            nrow = 1;
+            tdeg = LLONG_MAX;
+        } else {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(b.counter, kChunk);
+            base = __shfl_sync(kFull, base, 0);
+            if (base >= g.nrows) break;
+            rb = base;
+            nrow = (unsigned)min((unsigned long long)kChunk, g.nrows - base);
+            tdeg = heavy_deg;
+        }
+        strip(rb, nrow, tdeg);
     }
 }
 

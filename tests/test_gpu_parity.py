@@ -312,3 +312,25 @@ def test_wide_step_odd_and_max_widths(ctx, oracle, n, c):
     tau = oracle.default_step_size(g)
     for kw in [dict(method=GPA, max_iter=8), dict(method=FISTA, max_iter=8, step_size=50 * tau, fista_restart=True)]:
         assert_same_run(ctx.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+
+
+# ---- heavy-row first phase of k_sweep (power-law hubs scheduled first) -----------------------
+@pytest.mark.parametrize("c,vshards", [(32, 1), (20, 1), (64, 1), (32, 3), (8, 1), (3, 2)])
+def test_heavy_row_phase_bitwise(oracle, c, vshards, monkeypatch):
+    """FC_HEAVY_DEG=24 makes many rows of a small citation graph 'heavy' (processed
+    one per warp before the 32-row strips, and skipped by the strips, including
+    runs of consecutive heavy rows and heavy first/last rows of a strip)."""
+    monkeypatch.setenv("FC_HEAVY_DEG", "24")
+    g = fc.generate_citation(30_000, 400_000, seed=3)
+    x0 = oracle.init_random(g.n, c, 5)
+    t = capi.Context(0) if vshards == 1 else capi.Context(0, virtual_shards=vshards)
+    try:
+        t.upload(g)
+        for kw in [dict(method=GPA, max_iter=6), dict(method=FISTA, max_iter=8, fista_restart=True)]:
+            assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+        if vshards == 1:
+            xs, m = t.fused_column_pass(x0)
+            xs_o, m_o = oracle.fused_column_pass(x0, g)
+            assert np.array_equal(xs, xs_o) and m == m_o
+    finally:
+        t.close()
