@@ -159,6 +159,21 @@ int fc_solver_run(fc_ctx* ctx, uint64_t iterations);
 int fc_solver_sync(fc_ctx* ctx, int* done);
 int fc_solver_end(fc_ctx* ctx, double* x_out, fc_trace_record* trace, uint64_t trace_cap,
                   fc_solve_summary* out);
+/* Run the session's remaining iterations (same stop rule and pass budget as
+ * fc_solve), then fc_solver_end. */
+int fc_solver_finish(fc_ctx* ctx, double* x_out, fc_trace_record* trace, uint64_t trace_cap,
+                     fc_solve_summary* out);
+
+/* ---- checkpoint / resume (new) ---------------------------
+ * fc_solver_checkpoint waits for the enqueued iterations, then writes the whole
+ * session (device control state, trace so far, every iterate / sweep / Gram
+ * buffer the next iteration reads) to `path`.  fc_solver_resume loads it into a
+ * context holding the same similarity (n, nnz, frob_sq and shard layout are
+ * checked) and reopens the session: continuing with fc_solver_run/finish gives
+ * the same trace and membership, bit for bit, as the uninterrupted run.
+ * Single-rank contexts (virtual shards allowed). FC_IO on file errors. */
+int fc_solver_checkpoint(fc_ctx* ctx, const char* path);
+int fc_solver_resume(fc_ctx* ctx, const char* path);
 
 /* ---- instrumentation (bench.py) ------------------------------------------ */
 /* The CUDA stream every kernel and collective of ctx is enqueued on. */

@@ -71,6 +71,9 @@ SIGNATURES = {
     "fc_solver_run": (C.c_int, [C.c_void_p, C.c_uint64]),
     "fc_solver_sync": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     "fc_solver_end": (C.c_int, [C.c_void_p, _dp, C.POINTER(TraceRecordC), C.c_uint64, C.POINTER(SummaryC)]),
+    "fc_solver_finish": (C.c_int, [C.c_void_p, _dp, C.POINTER(TraceRecordC), C.c_uint64, C.POINTER(SummaryC)]),
+    "fc_solver_checkpoint": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "fc_solver_resume": (C.c_int, [C.c_void_p, C.c_char_p]),
     "fc_stream": (C.c_void_p, [C.c_void_p]),
     "fc_launch_count": (C.c_uint64, [C.c_void_p]),
     "fc_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
@@ -331,6 +334,24 @@ class Context:
         out = np.empty((n, c)) if want_x else None
         self._c(lib().fc_solver_end(self.h, _p(out), recs, cap, C.byref(summ)))
         return _result(out, recs, summ, cap)
+
+    def finish(self, n, c, want_x=True, trace_cap=None):
+        """fc_solver_finish: run the remaining iterations of the session, then end()."""
+        cap = trace_cap if trace_cap is not None else int(min(self._cfg.max_iter + 2, 1 << 20))
+        recs = (TraceRecordC * max(cap, 1))()
+        summ = SummaryC()
+        out = np.empty((n, c)) if want_x else None
+        self._c(lib().fc_solver_finish(self.h, _p(out), recs, cap, C.byref(summ)))
+        return _result(out, recs, summ, cap)
+
+    def checkpoint(self, path):
+        """fc_solver_checkpoint: save the running session to `path`."""
+        self._c(lib().fc_solver_checkpoint(self.h, os.fsencode(path)))
+
+    def resume(self, path, cfg: SolverConfigC):
+        """fc_solver_resume: reopen a saved session (cfg: the run's config, for trace sizing)."""
+        self._cfg = cfg
+        self._c(lib().fc_solver_resume(self.h, os.fsencode(path)))
 
     # ---- instrumentation ----------------------------------------------------
     def stream_ptr(self) -> int:

@@ -124,6 +124,8 @@ struct fc_ctx {
     uint64_t max_iter = 0;
     uint64_t enqueued = 0;             // iterations enqueued after begin
     uint64_t host_iter = 0;            // FISTA/GPA iteration index of the next enqueued pass
+    uint64_t bt_max_host = 0;          // session's backtracking cap (pass budget of fc_solve)
+    unsigned long long csr_fp = 0;     // fingerprint of the resident shard CSR
     cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
 
     bool sweep_tma = false;            // FC_SWEEP=tma selects the TMA gather4 sweep
@@ -1133,6 +1135,17 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
         }
     }
     ctx->local_nnz = lnnz;
+    {   // fingerprint of the shard CSR (checked by fc_solver_resume); before hot flags are set
+        unsigned long long* d_fp = nullptr;
+        CU(cudaMallocAsync(&d_fp, sizeof(unsigned long long), ctx->stream));
+        CU(cudaMemsetAsync(d_fp, 0, sizeof(unsigned long long), ctx->stream));
+        k_fingerprint<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(ctx->d_row_ptr, lrow, ctx->d_col,
+                                                                   weighted ? ctx->d_val : nullptr, lnnz, d_fp);
+        TRY(check_launch(ctx, "k_fingerprint"));
+        CU(cudaMemcpyAsync(&ctx->csr_fp, d_fp, sizeof ctx->csr_fp, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaFreeAsync(d_fp, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
     ctx->hot_threshold = 0xFFFFFFFFu;
     ctx->n = n;
     ctx->nnz = nnz;
@@ -1369,6 +1382,7 @@ int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const 
     ctx->max_iter = cfg->max_iter;
     ctx->enqueued = 0;
     ctx->host_iter = cfg->method == FC_GPA ? 0 : 1;
+    ctx->bt_max_host = cfg->bt_max;
     ctx->session = true;
     if (cfg->method != FC_GPA) TRY(enqueue_prelude(ctx));
     return FC_OK;
@@ -1428,21 +1442,20 @@ int fc_solver_end(fc_ctx* ctx, double* x_out, fc_trace_record* trace, uint64_t t
     return FC_OK;
 }
 
-// Whole solve with a one-chunk-behind stop check (identical decisions on every
-// rank, so every rank enqueues the same collectives).
-int fc_solve(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const double* x0, double* x_out,
-             fc_trace_record* trace, uint64_t trace_cap, fc_solve_summary* out) {
-    TRY(fc_solver_begin(ctx, cfg, c, x0));
-    const bool bt = cfg->method == FC_FISTA_BT;
-    const uint64_t passes = cfg->method == FC_GPA ? cfg->max_iter + 1 : cfg->max_iter;
-    const uint64_t limit = bt ? passes * ((uint64_t)cfg->bt_max + 1) : passes;
+// Enqueue the session's remaining passes in 8-pass chunks with a one-chunk-behind
+// stop check (identical decisions on every rank, so every rank enqueues the same
+// collectives).  Passes: max_iter (+1 for GPA's final loss), x (bt_max + 1) with
+// backtracking; the ones already enqueued (a resumed session) are not repeated.
+static int run_to_end(fc_ctx* ctx) {
+    const bool bt = ctx->method == FC_FISTA_BT;
+    const uint64_t passes = ctx->method == FC_GPA ? ctx->max_iter + 1 : ctx->max_iter;
+    const uint64_t limit = bt ? passes * ((uint64_t)ctx->bt_max_host + 1) : passes;
     const uint64_t chunk = 8;
-    uint64_t issued = 0, chunks = 0;
+    uint64_t chunks = 0;
     int pending = -1;
-    while (issued < limit) {
-        const uint64_t k = std::min(chunk, limit - issued);
+    while (ctx->enqueued < limit) {
+        const uint64_t k = std::min(chunk, limit - ctx->enqueued);
         TRY(fc_solver_run(ctx, k));
-        issued += k;
         const int slot = (int)(chunks++ & 1);
         CU(cudaMemcpyAsync(&ctx->h_done[slot], &ctx->d_state->done, sizeof(int), cudaMemcpyDeviceToHost,
                            ctx->stream));
@@ -1453,7 +1466,172 @@ int fc_solve(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const double*
         }
         pending = slot;
     }
+    return FC_OK;
+}
+
+int fc_solve(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const double* x0, double* x_out,
+             fc_trace_record* trace, uint64_t trace_cap, fc_solve_summary* out) {
+    TRY(fc_solver_begin(ctx, cfg, c, x0));
+    TRY(run_to_end(ctx));
     return fc_solver_end(ctx, x_out, trace, trace_cap, out);
+}
+
+int fc_solver_finish(fc_ctx* ctx, double* x_out, fc_trace_record* trace, uint64_t trace_cap, fc_solve_summary* out) {
+    if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
+    CU(cudaSetDevice(ctx->device));
+    TRY(run_to_end(ctx));
+    return fc_solver_end(ctx, x_out, trace, trace_cap, out);
+}
+
+// ---- checkpoint / resume of a solver session ------------------------
+}  // extern "C"
+
+namespace {
+struct CkptHeader {
+    char magic[8];
+    uint32_t abi, state_size, trace_rec_size, c;
+    uint32_t method, bt, vshards, pad;
+    uint64_t n, nnz, local_rows, local_blocks;
+    uint64_t max_iter, enqueued, host_iter, bt_max, n_records, trace_alloc;
+    double frob_s;
+    unsigned long long csr_fp;
+};
+constexpr char kCkptMagic[8] = {'F', 'C', 'C', 'K', 'P', 'T', '0', '1'};
+constexpr size_t kCkptChunk = size_t(64) << 20;
+
+int ckpt_io_err(fc_ctx* ctx, const char* what, const char* path) {
+    return set_err(ctx, FC_IO, "checkpoint: cannot %s %s", what, path);
+}
+
+int dump_dev(fc_ctx* ctx, FILE* f, const void* d, size_t bytes, std::vector<char>& buf, const char* path) {
+    for (size_t off = 0; off < bytes; off += kCkptChunk) {
+        const size_t nb = std::min(kCkptChunk, bytes - off);
+        TRY(d2h_big(ctx, buf.data(), (const char*)d + off, nb));
+        if (std::fwrite(buf.data(), 1, nb, f) != nb) return ckpt_io_err(ctx, "write", path);
+    }
+    return FC_OK;
+}
+
+int load_dev(fc_ctx* ctx, FILE* f, void* d, size_t bytes, std::vector<char>& buf, const char* path) {
+    for (size_t off = 0; off < bytes; off += kCkptChunk) {
+        const size_t nb = std::min(kCkptChunk, bytes - off);
+        if (std::fread(buf.data(), 1, nb, f) != nb) return set_err(ctx, FC_IO, "checkpoint: truncated file %s", path);
+        TRY(h2d_big(ctx, (char*)d + off, buf.data(), nb));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    return FC_OK;
+}
+
+// every device buffer a session carries from one iteration to the next, in file order
+template <class F>
+int for_session_buffers(fc_ctx* ctx, F&& f) {
+    const size_t N = ctx->n, c = ctx->c, L = ctx->local_rows, LB = ctx->local_blocks;
+    const unsigned np = npairs_of(ctx->c), nch = nchains_of(ctx->c);
+    for (int k = 0; k < 3; ++k) TRY(f((void*)ctx->d_U[k], N * c * sizeof(double)));
+    for (int k = 0; k < 4; ++k)
+        if (ctx->d_xs[k]) TRY(f((void*)ctx->d_xs[k], L * c * sizeof(double)));
+    for (int k = 0; k < 3; ++k)
+        if (ctx->bt_alloc && ctx->d_rowterm[k]) TRY(f((void*)ctx->d_rowterm[k], L * sizeof(double)));
+    TRY(f((void*)ctx->d_prod, L * sizeof(double)));
+    for (int k = 0; k < 2; ++k) TRY(f((void*)ctx->d_gpart[k], LB * np * sizeof(double)));
+    TRY(f((void*)ctx->d_spart, LB * kNumScal * sizeof(double)));
+    TRY(f((void*)ctx->d_totals, (ctx->vshards + 1) * nch * sizeof(double)));
+    TRY(f((void*)ctx->d_chain_in, nch * sizeof(double)));
+    for (int k = 0; k < 2; ++k) TRY(f((void*)ctx->d_gfull[k], c * c * sizeof(double)));
+    return FC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int fc_solver_checkpoint(fc_ctx* ctx, const char* path) {
+    if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
+    if (ctx->comm) return set_err(ctx, FC_INVALID, "checkpoint: needs a single-rank context");
+    CU(cudaSetDevice(ctx->device));
+    int done = 0;
+    TRY(session_done(ctx, &done));                          // all enqueued passes finished
+    CkptHeader h;
+    std::memset(&h, 0, sizeof h);
+    std::memcpy(h.magic, kCkptMagic, 8);
+    h.abi = FC_ABI_VERSION;
+    h.state_size = sizeof(DevState);
+    h.trace_rec_size = sizeof(fc_trace_record);
+    h.c = ctx->c;
+    h.method = (uint32_t)ctx->method;
+    h.bt = ctx->bt_alloc ? 1 : 0;
+    h.vshards = (uint32_t)ctx->vshards;
+    h.n = ctx->n;
+    h.nnz = ctx->nnz;
+    h.local_rows = ctx->local_rows;
+    h.local_blocks = ctx->local_blocks;
+    h.max_iter = ctx->max_iter;
+    h.enqueued = ctx->enqueued;
+    h.host_iter = ctx->host_iter;
+    h.bt_max = ctx->bt_max_host;
+    h.n_records = std::min<uint64_t>(ctx->h_state->n_records, ctx->trace_alloc);
+    h.trace_alloc = ctx->trace_alloc;
+    h.frob_s = ctx->frob_s;
+    h.csr_fp = ctx->csr_fp;
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return ckpt_io_err(ctx, "open", path);
+    std::vector<char> buf(kCkptChunk);
+    std::vector<fc_trace_record> tr(h.n_records);
+    int rc = FC_OK;
+    if (std::fwrite(&h, sizeof h, 1, f) != 1 || std::fwrite(ctx->h_state, sizeof(DevState), 1, f) != 1) {
+        rc = ckpt_io_err(ctx, "write", path);
+    }
+    if (!rc && h.n_records) {
+        rc = d2h(ctx, tr.data(), ctx->d_trace, h.n_records * sizeof(fc_trace_record));
+        if (!rc && cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = set_err(ctx, FC_DEVICE, "checkpoint: trace copy");
+        if (!rc && std::fwrite(tr.data(), sizeof(fc_trace_record), h.n_records, f) != h.n_records)
+            rc = ckpt_io_err(ctx, "write", path);
+    }
+    if (!rc) rc = for_session_buffers(ctx, [&](void* d, size_t bytes) { return dump_dev(ctx, f, d, bytes, buf, path); });
+    if (std::fclose(f) != 0 && !rc) rc = ckpt_io_err(ctx, "close", path);
+    return rc;
+}
+
+int fc_solver_resume(fc_ctx* ctx, const char* path) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    if (ctx->comm) return set_err(ctx, FC_INVALID, "checkpoint: needs a single-rank context");
+    CU(cudaSetDevice(ctx->device));
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return ckpt_io_err(ctx, "open", path);
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    CkptHeader h;
+    if (std::fread(&h, sizeof h, 1, f) != 1 || std::memcmp(h.magic, kCkptMagic, 8) != 0)
+        return set_err(ctx, FC_IO, "checkpoint: %s is not a solver checkpoint", path);
+    if (h.abi != FC_ABI_VERSION || h.state_size != sizeof(DevState) || h.trace_rec_size != sizeof(fc_trace_record))
+        return set_err(ctx, FC_IO, "checkpoint: %s was written by an incompatible library version", path);
+    if (!ctx->have_csr || h.n != ctx->n || h.nnz != ctx->nnz || h.frob_s != ctx->frob_s ||
+        h.vshards != (uint32_t)ctx->vshards || h.csr_fp != ctx->csr_fp)
+        return set_err(ctx, FC_INVALID, "checkpoint: the resident similarity / shard layout differs from the saved one");
+    ctx->session = false;
+    TRY(ensure_work(ctx, h.c, h.bt != 0));
+    if (h.local_rows != ctx->local_rows || h.local_blocks != ctx->local_blocks)
+        return set_err(ctx, FC_INVALID, "checkpoint: shard layout differs from the saved one");
+    TRY(ensure_trace(ctx, std::max<uint64_t>(h.trace_alloc, 1)));
+    DevState s;
+    if (std::fread(&s, sizeof s, 1, f) != 1) return set_err(ctx, FC_IO, "checkpoint: truncated file %s", path);
+    std::vector<fc_trace_record> tr(h.n_records);
+    if (h.n_records && std::fread(tr.data(), sizeof(fc_trace_record), h.n_records, f) != h.n_records)
+        return set_err(ctx, FC_IO, "checkpoint: truncated file %s", path);
+    std::vector<char> buf(kCkptChunk);
+    TRY(for_session_buffers(ctx, [&](void* d, size_t bytes) { return load_dev(ctx, f, d, bytes, buf, path); }));
+    if (h.n_records) TRY(h2d(ctx, ctx->d_trace, tr.data(), h.n_records * sizeof(fc_trace_record)));
+    s.trace_cap = ctx->trace_alloc;
+    TRY(upload_state(ctx, s));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->method = (int)h.method;
+    ctx->max_iter = h.max_iter;
+    ctx->enqueued = h.enqueued;
+    ctx->host_iter = h.host_iter;
+    ctx->bt_max_host = h.bt_max;
+    ctx->session = true;
+    return FC_OK;
 }
 
 // ---- instrumentation -----------------------------------------------------------------

@@ -1468,6 +1468,27 @@ __global__ void k_flag_hot(unsigned* col, unsigned long long nnz, const unsigned
 }
 
 // Device clock origin of TraceRecord::elapsed_ms.
+// Fingerprint of the resident CSR (checkpoint compatibility): sum over entries of
+// a mix of (position, column, value bits), order-sensitive through the position.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__global__ void k_fingerprint(const long long* row_ptr, unsigned long long rows, const unsigned* col,
+                              const double* val, unsigned long long nnz, unsigned long long* out) {
+    unsigned long long acc = 0;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < nnz; k += stride) {
+        unsigned long long v = val ? (unsigned long long)__double_as_longlong(val[k]) : 0x3FF0000000000000ULL;
+        acc += mix64(k * 0x9E3779B97F4A7C15ULL ^ ((unsigned long long)(col[k] & kIdxMask) << 1) ^ mix64(v));
+    }
+    for (unsigned long long r = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; r <= rows; r += stride)
+        acc += mix64(~(r * 0xD1B54A32D192ED03ULL) ^ (unsigned long long)row_ptr[r]);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
 __global__ void k_stamp(DevState* st) {
     long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
