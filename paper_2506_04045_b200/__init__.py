@@ -14,5 +14,6 @@ from .api import (
     generate_citation, generate_sbm, gpa_step, gpa_step_fused, init_membership, kReductionBlock, kVersion,
     loss_decomposed, project_simplex, read_membership_csv, resolve_step_size, run_fista, run_gpa,
     set_default_context, share_frob_sq, share_matrix, solve, splitmix64_doubles, splitmix64_stream, to_string,
-    validate_membership, write_membership_csv, write_trace_csv,
+    validate_membership, write_membership_csv, write_trace_csv, write_membership_binary, read_membership_binary,
+    write_similarity_binary, read_similarity_binary, from_triplets, build_similarity,
 )

@@ -20,7 +20,7 @@ from enum import IntEnum
 import numpy as np
 
 from . import capi
-from .errors import InvalidInput
+from .errors import InvalidInput, IoError
 from .similarity import SparseSimilarity
 
 kReductionBlock = 1024          # parallel.hpp:15
@@ -305,6 +305,76 @@ def read_membership_csv(text: str) -> np.ndarray:     # membership.hpp:151-194
     if not rows:
         raise InvalidInput("membership CSV: no data rows")
     return np.array(rows, dtype=np.float64)
+
+
+# ---- binary artifacts (new; same layouts as the C++ headers) -------
+_MEMB_MAGIC = b"FCMEMB01"
+_CSR_MAGIC = b"FCCSR001"
+
+
+def write_membership_binary(x: np.ndarray, path) -> None:
+    """"FCMEMB01", uint64 N, uint64 C, N*C float64 node-major (membership.hpp, new)."""
+    x = np.ascontiguousarray(x, dtype="<f8")
+    with open(path, "wb") as f:
+        f.write(_MEMB_MAGIC)
+        f.write(np.array(x.shape, dtype="<u8").tobytes())
+        x.tofile(f)
+
+
+def read_membership_binary(path) -> np.ndarray:
+    with open(path, "rb") as f:
+        if f.read(8) != _MEMB_MAGIC:
+            raise IoError("membership binary: bad magic")
+        hdr = np.frombuffer(f.read(16), dtype="<u8")
+        if hdr.size != 2 or hdr[0] == 0 or hdr[1] == 0:
+            raise IoError("membership binary: bad header")
+        n, c = int(hdr[0]), int(hdr[1])
+        x = np.fromfile(f, dtype="<f8", count=n * c)
+        if x.size != n * c:
+            raise IoError("membership binary: truncated data")
+    return x.reshape(n, c).astype(np.float64, copy=False)
+
+
+def write_similarity_binary(s: SparseSimilarity, path) -> None:
+    """"FCCSR001", n, nnz, flags, frob_sq, row_ptr, col[, values] (sparse.hpp, new)."""
+    with open(path, "wb") as f:
+        f.write(_CSR_MAGIC)
+        f.write(np.array([s.n, s.nnz], dtype="<u8").tobytes())
+        f.write(np.array([0 if s.values is None else 1, 0], dtype="<u4").tobytes())
+        f.write(np.array([s.frob_sq], dtype="<f8").tobytes())
+        s.row_ptr.astype("<i8", copy=False).tofile(f)
+        s.col_idx.astype("<u4", copy=False).tofile(f)
+        if s.values is not None:
+            s.values.astype("<f8", copy=False).tofile(f)
+
+
+def read_similarity_binary(path, validate: bool = True) -> SparseSimilarity:
+    with open(path, "rb") as f:
+        if f.read(8) != _CSR_MAGIC:
+            raise IoError("similarity binary: bad magic")
+        raw = f.read(32)
+        if len(raw) != 32:
+            raise IoError("similarity binary: bad header")
+        n, nnz = (int(v) for v in np.frombuffer(raw[:16], dtype="<u8"))
+        flags = int(np.frombuffer(raw[16:20], dtype="<u4")[0])
+        frob = float(np.frombuffer(raw[24:32], dtype="<f8")[0])
+        rp = np.fromfile(f, dtype="<i8", count=n + 1)
+        ci = np.fromfile(f, dtype="<u4", count=nnz)
+        vals = np.fromfile(f, dtype="<f8", count=nnz) if flags & 1 else None
+        if rp.size != n + 1 or ci.size != nnz or (vals is not None and vals.size != nnz):
+            raise IoError("similarity binary: truncated data")
+    if rp[0] != 0 or int(rp[-1]) != nnz:
+        raise IoError("similarity binary: row_ptr does not span [0, nnz)")
+    if n and np.any(np.diff(rp) < 0):
+        raise IoError("similarity binary: row_ptr not monotone")
+    if nnz and int(ci.max()) >= n:
+        raise IoError("similarity binary: column index out of range")
+    s = SparseSimilarity(n, rp, ci, vals)
+    if validate:
+        s._validate_symmetry()
+    if s.frob_sq != frob:
+        raise IoError("similarity binary: frob_sq does not match the stored values")
+    return s
 
 
 # ---- simplex.hpp -------------------------------------------------------------------

@@ -187,6 +187,39 @@ TEST(MembershipCsv, RoundTripsBitExactly) {
     EXPECT_TRUE(read_membership_csv(in) == x);
 }
 
+TEST(Artifacts, BinaryMembershipAndSimilarityRoundTrip) {
+    const auto x = init(41, 5, InitKind::kRandom, 3);
+    std::stringstream mb;
+    write_membership_binary(x, mb);
+    EXPECT_TRUE(read_membership_binary(mb) == x);
+    const auto s = seven();
+    std::stringstream sb;
+    s.save_binary(sb);
+    const auto t = SparseSimilarity::load_binary(sb);
+    EXPECT_EQ(t.size(), s.size());
+    EXPECT_EQ(t.nnz(), s.nnz());
+    EXPECT_DOUBLE_EQ(t.frob_sq(), s.frob_sq());
+    for (std::size_t j = 0; j < s.size(); ++j) {
+        EXPECT_EQ(t.col_rows(j).size(), s.col_rows(j).size());
+        for (std::size_t k = 0; k < s.col_rows(j).size(); ++k) EXPECT_EQ(t.col_rows(j)[k], s.col_rows(j)[k]);
+    }
+    bool threw = false;
+    try {
+        std::stringstream bad("FCCSR00X");
+        SparseSimilarity::load_binary(bad);
+    } catch (const IoError&) {
+        threw = true;
+    }
+    EXPECT_TRUE(threw);
+    // a solve on the reloaded similarity equals one on the original
+    SolverConfig c;
+    c.method = Method::kFista;
+    c.max_iter = 12;
+    const auto a = solve(uniform_x3(), s, c), b = solve(uniform_x3(), t, c);
+    EXPECT_TRUE(a.membership == b.membership);
+    EXPECT_DOUBLE_EQ(a.trace.final_loss, b.trace.final_loss);
+}
+
 int dump() {
     // seven_node goldens: name x0-kind seed method step max_iter restart trace_every
     struct Run { const char* name; InitKind k; std::uint64_t seed; Method m; double step; std::size_t it; bool rs; std::size_t te; };
