@@ -3,8 +3,8 @@
 // column products, gradient and loss terms, fused_column_pass, loss_decomposed.
 // Everything N-scaled runs on the device (libfuzzyclust_cuda.so); the C x C
 // value-type methods of ShareMatrix are plain host code.  The Hessian-vector
-// product and the dense N x N oracles (objective.hpp:182-329) belong to the
-// second-order path and are not part of this build.
+// product (objective.hpp:182-223) runs on the device too; the
+// dense N x N oracles (objective.hpp:225-329) are not part of this build.
 #pragma once
 
 #include <cmath>
@@ -86,22 +86,15 @@ inline ShareMatrix share_matrix(const DenseMatrix& x, unsigned /*workers*/ = 1) 
     return out;
 }
 
-/// A B^T (objective.hpp:61-90): the off-diagonal block of the Gram of the
-/// stacked 2C x N matrix [A; B] -- same per-entry products, same block order.
-inline ShareMatrix cross_share(const DenseMatrix& a, const DenseMatrix& b, unsigned workers = 1) {
+/// A B^T (objective.hpp:61-90) on the device: the off-diagonal block of the Gram of
+/// the stacked N x 2C matrix [A | B] -- same per-entry products, same block order.
+inline ShareMatrix cross_share(const DenseMatrix& a, const DenseMatrix& b, unsigned /*workers*/ = 1) {
     if (a.rows() != b.rows() || a.cols() != b.cols()) throw InvalidInput("cross_share: shape mismatch");
-    const std::size_t c = a.rows(), n = a.cols();
-    DenseMatrix st(2 * c, n);
-    for (std::size_t i = 0; i < n; ++i) {
-        for (std::size_t r = 0; r < c; ++r) {
-            st(r, i) = a(r, i);
-            st(c + r, i) = b(r, i);
-        }
-    }
-    const ShareMatrix g = share_matrix(st, workers);
-    ShareMatrix out(c);
-    for (std::size_t r = 0; r < c; ++r)
-        for (std::size_t s = 0; s < c; ++s) out(r, s) = g(r, c + s);
+    if (!detail::resident_size_is(a.cols())) detail::ensure_size(a.cols());
+    ShareMatrix out(a.rows());
+    auto& d = device::context();
+    device::check(fc_cross_share(d.ctx, static_cast<uint32_t>(a.rows()), a.data().data(), b.data().data(), out.raw()),
+                  d.ctx);
     return out;
 }
 
@@ -168,6 +161,28 @@ inline double loss_decomposed(const DenseMatrix& x, const SparseSimilarity& s, c
                               unsigned workers = 1) {
     const ColumnPass p = fused_column_pass(x, s, workers);
     return s.frob_sq() + share.frob_sq() - 2.0 * p.merge;
+}
+
+/// Hessian-vector product at xbar applied to v (objective.hpp:182-217), on the device:
+/// column i = -4 (V s_i - A x_i - A^T x_i - B v_i), A = cross_share(V, X), B = X X^T.
+inline DenseMatrix hessian_vector_product(const DenseMatrix& xbar, const DenseMatrix& v, const SparseSimilarity& s,
+                                          unsigned /*workers*/ = 1) {
+    if (xbar.rows() != v.rows() || xbar.cols() != v.cols()) throw InvalidInput("hessian_vector_product: shape mismatch");
+    if (s.size() != xbar.cols()) throw InvalidInput("hessian_vector_product: similarity size mismatch");
+    s.ensure_resident();
+    DenseMatrix out(xbar.rows(), xbar.cols());
+    auto& d = device::context();
+    device::check(fc_hessian_vector_product(d.ctx, static_cast<uint32_t>(xbar.rows()), xbar.data().data(),
+                                            v.data().data(), out.data().data()),
+                  d.ctx);
+    return out;
+}
+
+/// <H(xbar) v, v>_F (objective.hpp:219-223): the HVP on the device, then the
+/// reference's single sequential frob_inner over the storage order on the host.
+inline double quadratic_form(const DenseMatrix& xbar, const DenseMatrix& v, const SparseSimilarity& s,
+                             unsigned workers = 1) {
+    return frob_inner(hessian_vector_product(xbar, v, s, workers), v);
 }
 
 }  // namespace fuzzyclust

@@ -100,6 +100,18 @@ void fc_destroy(fc_ctx* ctx);
  * frob_sq is SparseSimilarity::frob_sq() (sum of v*v in stored order). */
 int fc_upload_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* row_ptr,
                   const uint32_t* col_idx, const double* values, double frob_sq);
+/* ---- second order (granular, single-rank) --------------- */
+/* cross_share(A, B) = A B^T (objective.hpp:61-90): g_out C x C row-major; A, B n x c
+ * node-major; c <= 128 (computed as the Gram of the stacked n x 2c matrix). */
+int fc_cross_share(fc_ctx* ctx, uint32_t c, const double* a, const double* b, double* g_out);
+/* hessian_vector_product(xbar, v, s) (objective.hpp:182-217) against the resident
+ * similarity: out_i = -4 (V s_i - A x_i - A^T x_i - B v_i), A = cross_share(V, X),
+ * B = share_matrix(X); x, v, out n x c node-major; c <= 128. */
+int fc_hessian_vector_product(fc_ctx* ctx, uint32_t c, const double* x, const double* v, double* out);
+/* frob_inner (dense.hpp:40-46) on the host: sum_k a[k] * b[k], strictly sequential
+ * (quadratic_form = frob_inner(HVP, V)). */
+double fc_frob_inner(const double* a, const double* b, uint64_t count);
+
 /* SparseSimilarity::from_triplets (sparse.hpp:28-62) on the device: triplets
  * (row i, column j, value; values NULL = all 1.0) are validated, sorted by
  * (column, row), checked for duplicates and exact symmetry (the reference's

@@ -81,6 +81,10 @@ class Oracle:
         L.fco_share_matrix.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
         L.fco_share_frob_sq.restype = C.c_double
         L.fco_share_frob_sq.argtypes = [_dp, C.c_size_t]
+        L.fco_cross_share.argtypes = [_dp, _dp, C.c_size_t, C.c_size_t, _dp]
+        L.fco_hessian_vector_product.argtypes = [_dp, _dp, C.c_size_t, C.c_void_p, _dp]
+        L.fco_frob_inner.restype = C.c_double
+        L.fco_frob_inner.argtypes = [_dp, _dp, C.c_size_t]
         L.fco_fused_column_pass.argtypes = [_dp, C.c_size_t, C.POINTER(_Csr), _dp, _dp]
         L.fco_loss_decomposed.restype = C.c_double
         L.fco_loss_decomposed.argtypes = [_dp, C.c_size_t, C.POINTER(_Csr), _dp]
@@ -130,6 +134,26 @@ class Oracle:
     def share_frob_sq(self, g):
         g = np.ascontiguousarray(g, dtype=np.float64)
         return self.lib.fco_share_frob_sq(_ptr(g), g.shape[0])
+
+    def cross_share(self, a, b):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        g = np.empty((a.shape[1], a.shape[1]))
+        self.lib.fco_cross_share(_ptr(a), _ptr(b), a.shape[1], a.shape[0], _ptr(g))
+        return g
+
+    def hessian_vector_product(self, x, v, graph):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty_like(x)
+        s = self.csr(graph)
+        self._check(self.lib.fco_hessian_vector_product(_ptr(x), _ptr(v), x.shape[1], C.byref(s), _ptr(out)))
+        return out
+
+    def frob_inner(self, a, b):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        return self.lib.fco_frob_inner(_ptr(a), _ptr(b), a.size)
 
     def fused_column_pass(self, x, graph):
         x = np.ascontiguousarray(x, dtype=np.float64)
@@ -221,6 +245,8 @@ class Reference:
         L.fcref_share_matrix.argtypes = [_dp, C.c_uint64, C.c_uint64, C.c_uint, _dp]
         L.fcref_fused_column_pass.argtypes = [C.c_void_p, _dp, C.c_uint64, C.c_uint, _dp, _dp]
         L.fcref_loss_decomposed.argtypes = [C.c_void_p, _dp, C.c_uint64, C.c_uint, _dp]
+        L.fcref_cross_share.argtypes = [_dp, _dp, C.c_uint64, C.c_uint64, C.c_uint, _dp]
+        L.fcref_hessian_vector_product.argtypes = [C.c_void_p, _dp, _dp, C.c_uint64, C.c_uint, _dp, _dp]
         L.fcref_gpa_step_fused.argtypes = [_dp, C.c_uint64, C.c_uint64, _dp, _dp, C.c_double, C.c_uint, _dp]
         L.fcref_default_step_size.restype = C.c_double
         L.fcref_default_step_size.argtypes = [C.c_void_p]
@@ -264,6 +290,13 @@ class Reference:
         x = np.ascontiguousarray(x, dtype=np.float64)
         g = np.empty((x.shape[1], x.shape[1]))
         self._check(self.lib.fcref_share_matrix(_ptr(x), x.shape[1], x.shape[0], workers, _ptr(g)))
+        return g
+
+    def cross_share(self, a, b, workers=1):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        g = np.empty((a.shape[1], a.shape[1]))
+        self._check(self.lib.fcref_cross_share(_ptr(a), _ptr(b), a.shape[1], a.shape[0], workers, _ptr(g)))
         return g
 
     def gpa_step_fused(self, x, g, xs, tau, workers=1):
@@ -314,6 +347,16 @@ class RefSimilarity:
         self.ref._check(self.ref.lib.fcref_fused_column_pass(self.h, _ptr(x), x.shape[1], workers, _ptr(xs),
                                                              C.byref(m)))
         return xs, m.value
+
+    def hessian_vector_product(self, x, v, workers=1):
+        """(HVP, quadratic_form) of the reference (objective.hpp:186-223)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty_like(x)
+        q = C.c_double()
+        self.ref._check(self.ref.lib.fcref_hessian_vector_product(self.h, _ptr(x), _ptr(v), x.shape[1], workers,
+                                                                  _ptr(out), C.byref(q)))
+        return out, q.value
 
     def loss_decomposed(self, x, workers=1):
         x = np.ascontiguousarray(x, dtype=np.float64)

@@ -146,6 +146,64 @@ void fco_share_matrix(const double* x, size_t c, size_t n, double* g) {
     free(acc);
 }
 
+/* objective.hpp:61-90: A B^T, per-1024-column-block partials summed in ascending order */
+void fco_cross_share(const double* a, const double* b, size_t c, size_t n, double* g) {
+    double* acc = (double*)malloc(c * c * sizeof(double));
+    memset(g, 0, c * c * sizeof(double));
+    for (size_t begin = 0; begin < n; begin += FCO_BLOCK) {
+        const size_t end = begin + FCO_BLOCK < n ? begin + FCO_BLOCK : n;
+        memset(acc, 0, c * c * sizeof(double));
+        for (size_t i = begin; i < end; ++i) {
+            const double* ca = a + i * c;
+            const double* cb = b + i * c;
+            for (size_t r = 0; r < c; ++r)
+                for (size_t q = 0; q < c; ++q) acc[r * c + q] += ca[r] * cb[q];
+        }
+        for (size_t k = 0; k < c * c; ++k) g[k] += acc[k];
+    }
+    free(acc);
+}
+
+/* objective.hpp:186-217: column i of -4 V (S - X^T X) + 4 X (V^T X + X^T V), i.e.
+ * -4 (V s_i - A x_i - A^T x_i - B v_i) with A = cross_share(V, X), B = share_matrix(X);
+ * ShareMatrix::apply / transpose_apply (objective.hpp:37-51) are sequential in l. */
+int fco_hessian_vector_product(const double* x, const double* v, size_t c, const fco_csr* s, double* out) {
+    const size_t n = (size_t)s->n;
+    double* A = (double*)malloc(c * c * sizeof(double));
+    double* B = (double*)malloc(c * c * sizeof(double));
+    double* vs = (double*)malloc(c * sizeof(double));
+    fco_cross_share(v, x, c, n, A);
+    fco_share_matrix(x, c, n, B);
+    for (size_t i = 0; i < n; ++i) {
+        for (size_t k = 0; k < c; ++k) vs[k] = 0.0;             /* similarity_column_product */
+        for (int64_t e = s->row_ptr[i]; e < s->row_ptr[i + 1]; ++e) {
+            const double* vj = v + (size_t)s->col_idx[e] * c;
+            const double w = s->values ? s->values[e] : 1.0;
+            for (size_t r = 0; r < c; ++r) vs[r] += w * vj[r];
+        }
+        const double* xi = x + i * c;
+        const double* vi = v + i * c;
+        for (size_t k = 0; k < c; ++k) {
+            double ax = 0.0, atx = 0.0, bv = 0.0;
+            for (size_t l = 0; l < c; ++l) ax += A[k * c + l] * xi[l];
+            for (size_t l = 0; l < c; ++l) atx += A[l * c + k] * xi[l];
+            for (size_t l = 0; l < c; ++l) bv += B[k * c + l] * vi[l];
+            out[i * c + k] = -4.0 * (vs[k] - ax - atx - bv);
+        }
+    }
+    free(A);
+    free(B);
+    free(vs);
+    return FCO_OK;
+}
+
+/* dense.hpp:40-46 frob_inner: one sequential sum over the storage order */
+double fco_frob_inner(const double* a, const double* b, size_t count) {
+    double acc = 0.0;
+    for (size_t k = 0; k < count; ++k) acc += a[k] * b[k];
+    return acc;
+}
+
 /* objective.hpp:25-29 */
 double fco_share_frob_sq(const double* g, size_t c) {
     double s = 0.0;

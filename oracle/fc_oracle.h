@@ -91,6 +91,12 @@ double fco_feasibility_error(const double* x, size_t c, size_t n);
 void fco_share_matrix(const double* x, size_t c, size_t n, double* g);
 /* objective.hpp:25-29 */
 double fco_share_frob_sq(const double* g, size_t c);
+/* objective.hpp:61-90 cross_share(A, B) = A B^T (C x C, row-major) */
+void fco_cross_share(const double* a, const double* b, size_t c, size_t n, double* g);
+/* objective.hpp:186-217 hessian_vector_product(xbar, v, s) (N x C, node-major) */
+int fco_hessian_vector_product(const double* x, const double* v, size_t c, const fco_csr* s, double* out);
+/* dense.hpp:40-46 frob_inner */
+double fco_frob_inner(const double* a, const double* b, size_t count);
 /* objective.hpp:151-173 -- xs is C x N column-major */
 int fco_fused_column_pass(const double* x, size_t c, const fco_csr* s, double* xs, double* merge);
 /* objective.hpp:176-180 */

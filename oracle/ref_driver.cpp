@@ -210,6 +210,26 @@ int fcref_fused_column_pass(void* h, const double* x, uint64_t c, unsigned worke
     });
 }
 
+int fcref_cross_share(const double* a, const double* b, uint64_t c, uint64_t n, unsigned workers, double* g) {
+    return guarded([&] {
+        const auto ma = wrap(a, c, n), mb = wrap(b, c, n);
+        const ShareMatrix s = cross_share(ma, mb, workers);
+        for (std::size_t r = 0; r < c; ++r)
+            for (std::size_t q = 0; q < c; ++q) g[r * c + q] = s(r, q);
+    });
+}
+
+int fcref_hessian_vector_product(void* h, const double* x, const double* v, uint64_t c, unsigned workers,
+                                 double* out, double* qform) {
+    return guarded([&] {
+        const auto& s = *static_cast<SparseSimilarity*>(h);
+        const auto mx = wrap(x, c, s.size()), mv = wrap(v, c, s.size());
+        const DenseMatrix hv = hessian_vector_product(mx, mv, s, workers);
+        std::memcpy(out, hv.data().data(), hv.data().size() * sizeof(double));
+        if (qform) *qform = quadratic_form(mx, mv, s, workers);
+    });
+}
+
 int fcref_loss_decomposed(void* h, const double* x, uint64_t c, unsigned workers, double* loss) {
     return guarded([&] {
         const auto& s = *static_cast<SparseSimilarity*>(h);

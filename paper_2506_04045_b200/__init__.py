@@ -16,4 +16,5 @@ from .api import (
     set_default_context, share_frob_sq, share_matrix, solve, splitmix64_doubles, splitmix64_stream, to_string,
     validate_membership, write_membership_csv, write_trace_csv, write_membership_binary, read_membership_binary,
     write_similarity_binary, read_similarity_binary, from_triplets, build_similarity,
+    cross_share, hessian_vector_product, quadratic_form, frob_inner,
 )

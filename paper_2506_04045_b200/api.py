@@ -307,6 +307,34 @@ def read_membership_csv(text: str) -> np.ndarray:     # membership.hpp:151-194
     return np.array(rows, dtype=np.float64)
 
 
+# ---- second order (objective.hpp:61-90, :182-223) ------------------
+def cross_share(a: np.ndarray, b: np.ndarray, workers: int = 1, ctx: capi.Context | None = None) -> np.ndarray:
+    """A B^T on the device (Gram of the stacked [A | B])."""
+    if a.shape != b.shape:
+        raise InvalidInput("cross_share: shape mismatch")
+    return _ctx_for(None, ctx, n=a.shape[0]).cross_share(a, b)
+
+
+def hessian_vector_product(xbar: np.ndarray, v: np.ndarray, s: SparseSimilarity, workers: int = 1,
+                           ctx: capi.Context | None = None) -> np.ndarray:
+    if xbar.shape != v.shape:
+        raise InvalidInput("hessian_vector_product: shape mismatch")
+    if s.size() != xbar.shape[0]:
+        raise InvalidInput("hessian_vector_product: similarity size mismatch")
+    return _ctx_for(s, ctx).hessian_vector_product(xbar, v)
+
+
+def frob_inner(a: np.ndarray, b: np.ndarray) -> float:
+    """dense.hpp:40-46: one sequential sum over the storage order (host loop in the library)."""
+    return capi.frob_inner(a, b)
+
+
+def quadratic_form(xbar: np.ndarray, v: np.ndarray, s: SparseSimilarity, workers: int = 1,
+                   ctx: capi.Context | None = None) -> float:
+    """<H(xbar) v, v>_F: device HVP, then the reference's sequential frob_inner on the host."""
+    return frob_inner(hessian_vector_product(xbar, v, s, workers, ctx), v)
+
+
 # ---- binary artifacts (new, SURVEY.md 8(d) / 8(f)4; same layouts as the C++ headers) -------
 _MEMB_MAGIC = b"FCMEMB01"
 _CSR_MAGIC = b"FCCSR001"

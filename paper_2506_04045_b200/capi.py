@@ -83,6 +83,9 @@ SIGNATURES = {
     "fc_build_from_triplets": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _u32p, _u32p, _dp, _i64p, _u32p, _dp,
                                          _dp, C.POINTER(C.c_int)]),
     "fc_build_similarity": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _u32p, _i64p, _u32p, _dp]),
+    "fc_cross_share": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp]),
+    "fc_hessian_vector_product": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp]),
+    "fc_frob_inner": (C.c_double, [_dp, _dp, C.c_uint64]),
     "fc_free": (None, [C.c_void_p]),
 }
 
@@ -145,6 +148,14 @@ def generate_graph(kind: int, n: int, m: int, seed: int, *, blocks: int = 16, p_
     return row_ptr, col_idx
 
 
+def frob_inner(a, b) -> float:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError("frob_inner: shape mismatch")
+    return float(lib().fc_frob_inner(_p(a), _p(b), a.size))
+
+
 class Context:
     """One device (one process per GPU).  world > 1: NCCL row-sharded solver."""
 
@@ -192,6 +203,20 @@ class Context:
             self._graph_ref = weakref.ref(graph)
         except TypeError:
             self._graph_ref = None
+
+    def cross_share(self, a, b):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        g = np.empty((a.shape[1], a.shape[1]))
+        self._c(lib().fc_cross_share(self.h, a.shape[1], _p(a), _p(b), _p(g)))
+        return g
+
+    def hessian_vector_product(self, x, v):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty_like(x)
+        self._c(lib().fc_hessian_vector_product(self.h, x.shape[1], _p(x), _p(v), _p(out)))
+        return out
 
     def build_from_triplets(self, n, rows, cols, values=None):
         """fc_build_from_triplets: device from_triplets; the result is resident and returned."""

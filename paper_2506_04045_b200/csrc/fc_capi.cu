@@ -739,6 +739,9 @@ int enqueue_gpa_iteration(fc_ctx* ctx) {
 }
 
 int upload_state(fc_ctx* ctx, const DevState& s) {
+    // h_state is the pinned source of the async copy: a previous upload still queued
+    // on the stream would read the new contents, so drain the stream first
+    CU(cudaStreamSynchronize(ctx->stream));
     *ctx->h_state = s;
     CU(cudaMemcpyAsync(ctx->d_state, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
     return FC_OK;
@@ -1206,6 +1209,66 @@ int fc_fused_column_pass(fc_ctx* ctx, uint32_t c, const double* x, double* xs_ou
     TRY(h2d_big(ctx, ctx->d_U[0], x, ctx->n * c * sizeof(double)));
     TRY(pass_on_u0(ctx, c, merge_out));
     if (xs_out) TRY(d2h_big(ctx, xs_out, ctx->d_xs[0], ctx->n * c * sizeof(double)));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return FC_OK;
+}
+
+// ---- second order ---------------------------------------------------
+// Gram of Z = [A | B] (2c wide) into gfull[0]; U[1] = A, U[2] = B (n x c each).
+static int stacked_gram(fc_ctx* ctx, uint32_t c, const double* a, const double* b) {
+    if (c == 0 || c > 128) return set_err(ctx, FC_INVALID, "cross_share: C=%u outside [1, 128]", c);
+    TRY(ensure_work(ctx, 2 * c, false));
+    const size_t nc = ctx->n * c;
+    TRY(h2d_big(ctx, ctx->d_U[1], a, nc * sizeof(double)));
+    TRY(h2d_big(ctx, ctx->d_U[2], b, nc * sizeof(double)));
+    k_stack2<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(ctx->d_U[1], ctx->d_U[2], ctx->d_U[0], ctx->n, (int)c);
+    TRY(check_launch(ctx, "k_stack2"));
+    DevState s = base_state(ctx);
+    s.sw_b = 0;
+    TRY(upload_state(ctx, s));
+    TRY(phase_gram(ctx, false));
+    TRY(phase_combine(ctx, 1, 0));
+    TRY(phase_finalize(ctx, kFinGranular, 1));
+    return FC_OK;
+}
+
+int fc_cross_share(fc_ctx* ctx, uint32_t c, const double* a, const double* b, double* g_out) {
+    if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
+    CU(cudaSetDevice(ctx->device));
+    TRY(stacked_gram(ctx, c, a, b));
+    std::vector<double> g2((size_t)4 * c * c);
+    TRY(d2h(ctx, g2.data(), ctx->d_gfull[0], g2.size() * sizeof(double)));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (uint32_t r = 0; r < c; ++r)
+        for (uint32_t q = 0; q < c; ++q) g_out[(size_t)r * c + q] = g2[(size_t)r * 2 * c + c + q];
+    return FC_OK;
+}
+
+int fc_hessian_vector_product(fc_ctx* ctx, uint32_t c, const double* x, const double* v, double* out) {
+    if (!granular_ok(ctx)) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
+    CU(cudaSetDevice(ctx->device));
+    TRY(stacked_gram(ctx, c, v, x));                         // A = cross_share(V, X), B = share_matrix(X)
+    // V s_i for every node: single sweep over U[1] (= V) with row width c
+    DevState s = base_state(ctx);
+    s.sw_b = 1;
+    s.xs_w = 0;
+    TRY(upload_state(ctx, s));
+    CU(cudaMemsetAsync(ctx->d_counter, 0, ctx->shards.size() * sizeof(unsigned), ctx->stream));
+    CU(cudaMemsetAsync(ctx->d_counter + 64, 0, ctx->shards.size() * sizeof(unsigned), ctx->stream));
+    for (size_t sh = 0; sh < ctx->shards.size(); ++sh) {
+        Bufs b = make_bufs(ctx, sh);
+        for (int k = 0; k < 4; ++k)
+            if (ctx->d_xs[k]) b.xs[k] = ctx->d_xs[k] + ctx->shards[sh].lrow * c;
+        Geo g = make_geo(ctx, sh);
+        g.C = c;
+        g.npairs = npairs_of(c);
+        TRY(by_c<LaunchSweep>(ctx, c, ctx, b, g, false));
+    }
+    const double* vs = ctx->d_xs[kMatExt];                    // xs set 0, slot kMatExt (single sweep)
+    k_hvp_rows<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(ctx->d_gfull[0], vs, ctx->d_U[2], ctx->d_U[1],
+                                                           ctx->d_U[0], ctx->n, (int)c);
+    TRY(check_launch(ctx, "k_hvp_rows"));
+    TRY(d2h_big(ctx, out, ctx->d_U[0], ctx->n * c * sizeof(double)));
     CU(cudaStreamSynchronize(ctx->stream));
     return FC_OK;
 }

@@ -1468,6 +1468,39 @@ __global__ void k_flag_hot(unsigned* col, unsigned long long nnz, const unsigned
 }
 
 // Device clock origin of TraceRecord::elapsed_ms.
+// ---- second order (objective.hpp:61-90, :186-217) ------------------------------------
+// Z = [A | B] row by row (N x 2C): the Gram of Z holds cross_share(A, B) = A B^T in its
+// upper-right C x C block with exactly the reference's per-block products and order.
+__global__ void k_stack2(const double* a, const double* b, double* z, unsigned long long n, int C) {
+    const unsigned long long total = n * (unsigned long long)(2 * C);
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long i = e / (2 * C);
+        const int k = (int)(e - i * 2 * C);
+        z[e] = k < C ? a[i * C + k] : b[i * C + (k - C)];
+    }
+}
+
+// out_i[k] = -4 (vs[k] - ax[k] - atx[k] - bv[k]); g2 = the 2C x 2C Gram of [V | X]:
+// A[k][l] = g2[k][C+l], B[k][l] = g2[C+k][C+l]; each sum sequential in l from 0.0.
+__global__ void k_hvp_rows(const double* g2, const double* vs, const double* x, const double* v, double* out,
+                           unsigned long long n, int C) {
+    const unsigned long long total = n * (unsigned long long)C;
+    const int W = 2 * C;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long i = e / C;
+        const int k = (int)(e - i * C);
+        const double* xi = x + i * C;
+        const double* vi = v + i * C;
+        double ax = 0.0, atx = 0.0, bv = 0.0;
+        for (int l = 0; l < C; ++l) ax = dadd(ax, dmul(g2[k * W + C + l], xi[l]));
+        for (int l = 0; l < C; ++l) atx = dadd(atx, dmul(g2[l * W + C + k], xi[l]));
+        for (int l = 0; l < C; ++l) bv = dadd(bv, dmul(g2[(C + k) * W + C + l], vi[l]));
+        out[e] = dmul(-4.0, dsub(dsub(dsub(vs[e], ax), atx), bv));
+    }
+}
+
 // Fingerprint of the resident CSR (checkpoint compatibility): sum over entries of
 // a mix of (position, column, value bits), order-sensitive through the position.
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {

@@ -225,3 +225,11 @@ extern "C" int fc_generate_graph_impl(const fc_graph_spec* spec, uint64_t* nnz_o
     *col_idx_out = ci;
     return FC_OK;
 }
+
+// dense.hpp:40-46 frob_inner: one sequential sum over the storage order (host; the
+// order is the contract, so it is not parallelised).  Compiled without FMA contraction.
+extern "C" double fc_frob_inner(const double* a, const double* b, uint64_t count) {
+    double acc = 0.0;
+    for (uint64_t k = 0; k < count; ++k) acc += a[k] * b[k];
+    return acc;
+}

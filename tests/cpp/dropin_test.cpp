@@ -220,6 +220,23 @@ TEST(Artifacts, BinaryMembershipAndSimilarityRoundTrip) {
     EXPECT_DOUBLE_EQ(a.trace.final_loss, b.trace.final_loss);
 }
 
+TEST(SecondOrder, HessianVectorProductOnSevenNode) {
+    // objective_test.cpp style: <H u, v> == <u, H v> (H symmetric) and q = <H v, v>
+    const auto s = seven();
+    const auto x = init(7, 2, InitKind::kRandom, 5);
+    DenseMatrix u(2, 7), v(2, 7);
+    SplitMix64 r(9);
+    for (double& e : u.data()) e = r.next_double() - 0.5;
+    for (double& e : v.data()) e = r.next_double() - 0.5;
+    const auto hu = hessian_vector_product(x, u, s), hv = hessian_vector_product(x, v, s);
+    EXPECT_NEAR(frob_inner(hu, v), frob_inner(u, hv), 1e-12);
+    EXPECT_DOUBLE_EQ(quadratic_form(x, v, s), frob_inner(hv, v));
+    const auto a = cross_share(u, x);
+    double a01 = 0.0;
+    for (std::size_t i = 0; i < 7; ++i) a01 += u(0, i) * x(1, i);
+    EXPECT_DOUBLE_EQ(a(0, 1), a01);
+}
+
 int dump() {
     // seven_node goldens: name x0-kind seed method step max_iter restart trace_every
     struct Run { const char* name; InitKind k; std::uint64_t seed; Method m; double step; std::size_t it; bool rs; std::size_t te; };
