@@ -112,6 +112,30 @@ int fc_hessian_vector_product(fc_ctx* ctx, uint32_t c, const double* x, const do
  * (quadratic_form = frob_inner(HVP, V)). */
 double fc_frob_inner(const double* a, const double* b, uint64_t count);
 
+/* ---- edge-list ingest ----------------------------------- */
+typedef struct fc_ingest_result {
+    uint64_t parsed_nodes;   /* nodes after parse_edge_list */
+    uint64_t lcc_nodes;      /* nodes of the largest connected component (stages >= 1) */
+    uint64_t num_nodes;      /* nodes of the returned graph */
+    uint64_t num_edges;      /* edges of the returned graph */
+    uint32_t* edges;         /* 2 * num_edges ids, (u < v) pairs sorted ascending; fc_free */
+    int64_t* original_ids;   /* num_nodes input ids of the returned nodes; fc_free */
+} fc_ingest_result;
+/* The reference's load_pipeline (tools/fuzzyclust.cpp:62-89) on `len` bytes of
+ * "u v" text: stages 0 = parse_edge_list only (graph.hpp:63-103, ids compacted by
+ * first appearance, self-loops / duplicates dropped, symmetrised), 1 = + largest
+ * connected component (graph.hpp:146-175, ties to the smallest id), 2 = + 2-core
+ * (graph.hpp:185-219).  Parse errors: FC_IO with the reference's messages and line
+ * numbers ("edge list is empty" when no edge line). */
+int fc_ingest_edge_list(fc_ctx* ctx, const char* text, uint64_t len, int stages, fc_ingest_result* out);
+/* largest_connected_component_nodes / two_core_nodes (graph.hpp:146-169, :206-213)
+ * of a Graph given as its edge list (2 * num_edges ids); *nodes_out (ascending,
+ * malloc'ed: fc_free) and *count. */
+int fc_graph_lcc_nodes(fc_ctx* ctx, uint64_t num_nodes, uint64_t num_edges, const uint32_t* edges,
+                       uint32_t** nodes_out, uint64_t* count);
+int fc_graph_two_core_nodes(fc_ctx* ctx, uint64_t num_nodes, uint64_t num_edges, const uint32_t* edges,
+                            uint32_t** nodes_out, uint64_t* count);
+
 /* SparseSimilarity::from_triplets (sparse.hpp:28-62) on the device: triplets
  * (row i, column j, value; values NULL = all 1.0) are validated, sorted by
  * (column, row), checked for duplicates and exact symmetry (the reference's

@@ -245,6 +245,12 @@ class Reference:
         L.fcref_share_matrix.argtypes = [_dp, C.c_uint64, C.c_uint64, C.c_uint, _dp]
         L.fcref_fused_column_pass.argtypes = [C.c_void_p, _dp, C.c_uint64, C.c_uint, _dp, _dp]
         L.fcref_loss_decomposed.argtypes = [C.c_void_p, _dp, C.c_uint64, C.c_uint, _dp]
+        L.fcref_load_pipeline.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(C.c_uint64),
+                                          C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                          C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.POINTER(C.c_int64))]
+        L.fcref_graph_nodes.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint32), C.c_int,
+                                        C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64)]
+        L.fcref_free_buf.argtypes = [C.c_void_p]
         L.fcref_cross_share.argtypes = [_dp, _dp, C.c_uint64, C.c_uint64, C.c_uint, _dp]
         L.fcref_hessian_vector_product.argtypes = [C.c_void_p, _dp, _dp, C.c_uint64, C.c_uint, _dp, _dp]
         L.fcref_gpa_step_fused.argtypes = [_dp, C.c_uint64, C.c_uint64, _dp, _dp, C.c_double, C.c_uint, _dp]
@@ -291,6 +297,30 @@ class Reference:
         g = np.empty((x.shape[1], x.shape[1]))
         self._check(self.lib.fcref_share_matrix(_ptr(x), x.shape[1], x.shape[0], workers, _ptr(g)))
         return g
+
+    def load_pipeline(self, text: bytes, stages: int = 2):
+        """(parsed_nodes, lcc_nodes, num_nodes, edges (m, 2) uint32, original_ids) of the reference."""
+        pn, ln, nn, ne = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        e = C.POINTER(C.c_uint32)()
+        ids = C.POINTER(C.c_int64)()
+        self._check(self.lib.fcref_load_pipeline(text, len(text), stages, C.byref(pn), C.byref(ln), C.byref(nn),
+                                                 C.byref(ne), C.byref(e), C.byref(ids)))
+        edges = np.ctypeslib.as_array(e, shape=(max(1, 2 * ne.value),))[: 2 * ne.value].copy().reshape(-1, 2)
+        orig = np.ctypeslib.as_array(ids, shape=(max(1, nn.value),))[: nn.value].copy()
+        self.lib.fcref_free_buf(C.cast(e, C.c_void_p))
+        self.lib.fcref_free_buf(C.cast(ids, C.c_void_p))
+        return pn.value, ln.value, nn.value, edges, orig
+
+    def graph_nodes(self, n, edges, which):
+        """which 0: largest_connected_component_nodes, 1: two_core_nodes."""
+        e = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1)
+        out = C.POINTER(C.c_uint32)()
+        cnt = C.c_uint64()
+        self._check(self.lib.fcref_graph_nodes(n, e.size // 2, e.ctypes.data_as(C.POINTER(C.c_uint32)), which,
+                                               C.byref(out), C.byref(cnt)))
+        v = np.ctypeslib.as_array(out, shape=(max(1, cnt.value),))[: cnt.value].copy()
+        self.lib.fcref_free_buf(C.cast(out, C.c_void_p))
+        return v
 
     def cross_share(self, a, b, workers=1):
         a = np.ascontiguousarray(a, dtype=np.float64)

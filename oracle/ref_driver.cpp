@@ -230,6 +230,59 @@ int fcref_hessian_vector_product(void* h, const double* x, const double* v, uint
     });
 }
 
+// tools/fuzzyclust.cpp:62-89 load_pipeline, composed from the reference's graph.hpp
+// (parse_edge_list -> largest_connected_component_nodes -> induced_subgraph ->
+// two_core_nodes -> induced_subgraph).  Outputs malloc'ed; fcref_free_buf.
+int fcref_load_pipeline(const char* text, uint64_t len, int stages, uint64_t* parsed_nodes, uint64_t* lcc_nodes,
+                        uint64_t* num_nodes, uint64_t* num_edges, uint32_t** edges, int64_t** ids) {
+    return guarded([&] {
+        std::istringstream in(std::string(text, len));
+        auto parsed = parse_edge_list(in);
+        Graph g = parsed.graph;
+        std::vector<std::int64_t> orig = parsed.original_ids;
+        *parsed_nodes = g.num_nodes;
+        *lcc_nodes = 0;
+        if (stages >= 1) {
+            const auto lcc = largest_connected_component_nodes(g);
+            g = induced_subgraph(g, lcc);
+            std::vector<std::int64_t> kept;
+            for (std::uint32_t v : lcc) kept.push_back(orig[v]);
+            orig = kept;
+            *lcc_nodes = g.num_nodes;
+            if (stages >= 2) {
+                const auto core = two_core_nodes(g);
+                g = induced_subgraph(g, core);
+                std::vector<std::int64_t> surv;
+                for (std::uint32_t v : core) surv.push_back(orig[v]);
+                orig = surv;
+            }
+        }
+        *num_nodes = g.num_nodes;
+        *num_edges = g.edges.size();
+        *edges = static_cast<uint32_t*>(std::malloc(std::max<std::size_t>(2 * g.edges.size(), 1) * 4));
+        *ids = static_cast<int64_t*>(std::malloc(std::max<std::size_t>(orig.size(), 1) * 8));
+        for (std::size_t k = 0; k < g.edges.size(); ++k) {
+            (*edges)[2 * k] = g.edges[k].first;
+            (*edges)[2 * k + 1] = g.edges[k].second;
+        }
+        std::copy(orig.begin(), orig.end(), *ids);
+    });
+}
+
+int fcref_graph_nodes(uint64_t n, uint64_t m, const uint32_t* edges, int which, uint32_t** nodes, uint64_t* count) {
+    return guarded([&] {
+        Graph g;
+        g.num_nodes = n;
+        for (uint64_t k = 0; k < m; ++k) g.edges.emplace_back(edges[2 * k], edges[2 * k + 1]);
+        const auto v = which == 0 ? largest_connected_component_nodes(g) : two_core_nodes(g);
+        *nodes = static_cast<uint32_t*>(std::malloc(std::max<std::size_t>(v.size(), 1) * 4));
+        std::copy(v.begin(), v.end(), *nodes);
+        *count = v.size();
+    });
+}
+
+void fcref_free_buf(void* p) { std::free(p); }
+
 int fcref_loss_decomposed(void* h, const double* x, uint64_t c, unsigned workers, double* loss) {
     return guarded([&] {
         const auto& s = *static_cast<SparseSimilarity*>(h);

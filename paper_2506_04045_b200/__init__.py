@@ -17,4 +17,6 @@ from .api import (
     validate_membership, write_membership_csv, write_trace_csv, write_membership_binary, read_membership_binary,
     write_similarity_binary, read_similarity_binary, from_triplets, build_similarity,
     cross_share, hessian_vector_product, quadratic_form, frob_inner,
+    Graph, ParsedGraph, LoadedGraph, parse_edge_list, largest_connected_component_nodes, two_core_nodes,
+    induced_subgraph, largest_connected_component, prune_degree_one, load_pipeline, write_edge_list,
 )

@@ -307,6 +307,88 @@ def read_membership_csv(text: str) -> np.ndarray:     # membership.hpp:151-194
     return np.array(rows, dtype=np.float64)
 
 
+# ---- graph.hpp / tools load_pipeline on the device -----------------
+@dataclass
+class Graph:                         # graph.hpp:21-42
+    num_nodes: int
+    edges: np.ndarray                # (m, 2) uint32, u < v, sorted, unique
+
+    def degrees(self) -> np.ndarray:
+        return np.bincount(self.edges.reshape(-1), minlength=self.num_nodes)
+
+
+@dataclass
+class ParsedGraph:                   # graph.hpp:53-58
+    graph: Graph
+    original_ids: np.ndarray
+
+
+@dataclass
+class LoadedGraph:                   # tools/fuzzyclust.cpp:52-58
+    graph: Graph
+    original_ids: np.ndarray
+    parsed_nodes: int
+    lcc_nodes: int
+
+
+def _text_bytes(text) -> bytes:
+    return text.encode() if isinstance(text, str) else bytes(text)
+
+
+def parse_edge_list(text, ctx: capi.Context | None = None) -> ParsedGraph:
+    """graph.hpp:63-103 (ids compacted by first appearance on the device)."""
+    r = (ctx or default_context()).ingest(_text_bytes(text), 0)
+    return ParsedGraph(Graph(r["num_nodes"], r["edges"]), r["original_ids"])
+
+
+def largest_connected_component_nodes(g: Graph, ctx: capi.Context | None = None) -> np.ndarray:
+    """graph.hpp:146-169: ascending; ties to the component holding the smallest id."""
+    return (ctx or default_context()).lcc_nodes(g.num_nodes, g.edges)
+
+
+def two_core_nodes(g: Graph, ctx: capi.Context | None = None) -> np.ndarray:
+    """graph.hpp:206-213: nodes surviving iterated degree <= 1 removal, ascending."""
+    return (ctx or default_context()).two_core_nodes(g.num_nodes, g.edges)
+
+
+def induced_subgraph(g: Graph, nodes) -> Graph:
+    """graph.hpp:107-120 (order-preserving recompaction; host)."""
+    nodes = np.asarray(nodes, dtype=np.int64)
+    new_id = np.full(g.num_nodes, -1, dtype=np.int64)
+    new_id[nodes] = np.arange(nodes.size)
+    e = g.edges.astype(np.int64)
+    keep = (new_id[e[:, 0]] >= 0) & (new_id[e[:, 1]] >= 0) if e.size else np.zeros(0, bool)
+    sub = new_id[e[keep]].astype(np.uint32).reshape(-1, 2)
+    return Graph(int(nodes.size), sub)
+
+
+def largest_connected_component(g: Graph, ctx: capi.Context | None = None) -> Graph:
+    return induced_subgraph(g, largest_connected_component_nodes(g, ctx))
+
+
+def prune_degree_one(g: Graph, ctx: capi.Context | None = None) -> Graph:
+    return induced_subgraph(g, two_core_nodes(g, ctx))
+
+
+def load_pipeline(text=None, path=None, prune: bool = True, ctx: capi.Context | None = None) -> LoadedGraph:
+    """tools/fuzzyclust.cpp:62-89: parse -> LCC -> optional 2-core, all on the device."""
+    if path is not None:
+        try:
+            with open(path, "rb") as f:
+                text = f.read()
+        except OSError:
+            raise IoError(f"cannot open {path}") from None
+    r = (ctx or default_context()).ingest(_text_bytes(text), 2 if prune else 1)
+    if r["num_nodes"] == 0:
+        raise InvalidInput("graph is empty after preprocessing")
+    return LoadedGraph(Graph(r["num_nodes"], r["edges"]), r["original_ids"], r["parsed_nodes"], r["lcc_nodes"])
+
+
+def write_edge_list(g: Graph) -> str:
+    """graph.hpp:222-224: "u v" lines in (u, v) order."""
+    return "".join(f"{u} {v}\n" for u, v in g.edges.tolist())
+
+
 # ---- second order (objective.hpp:61-90, :182-223; SURVEY.md 8(f)3) ------------------
 def cross_share(a: np.ndarray, b: np.ndarray, workers: int = 1, ctx: capi.Context | None = None) -> np.ndarray:
     """A B^T on the device (Gram of the stacked [A | B])."""

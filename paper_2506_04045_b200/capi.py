@@ -86,6 +86,11 @@ SIGNATURES = {
     "fc_cross_share": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp]),
     "fc_hessian_vector_product": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp]),
     "fc_frob_inner": (C.c_double, [_dp, _dp, C.c_uint64]),
+    "fc_ingest_edge_list": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int, C.c_void_p]),
+    "fc_graph_lcc_nodes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _u32p, C.POINTER(_u32p),
+                                     C.POINTER(C.c_uint64)]),
+    "fc_graph_two_core_nodes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _u32p, C.POINTER(_u32p),
+                                          C.POINTER(C.c_uint64)]),
     "fc_free": (None, [C.c_void_p]),
 }
 
@@ -156,6 +161,18 @@ def frob_inner(a, b) -> float:
     return float(lib().fc_frob_inner(_p(a), _p(b), a.size))
 
 
+class IngestResultC(C.Structure):
+    _fields_ = [("parsed_nodes", C.c_uint64), ("lcc_nodes", C.c_uint64), ("num_nodes", C.c_uint64),
+                ("num_edges", C.c_uint64), ("edges", C.POINTER(C.c_uint32)), ("original_ids", C.POINTER(C.c_int64))]
+
+
+def _take(ptr, count, dtype):
+    """Copy `count` items out of a library-malloc'ed buffer and free it."""
+    arr = np.ctypeslib.as_array(ptr, shape=(max(1, count),))[:count].astype(dtype, copy=True)
+    lib().fc_free(C.cast(ptr, C.c_void_p))
+    return arr
+
+
 class Context:
     """One device (one process per GPU).  world > 1: NCCL row-sharded solver."""
 
@@ -203,6 +220,28 @@ class Context:
             self._graph_ref = weakref.ref(graph)
         except TypeError:
             self._graph_ref = None
+
+    # ---- edge-list ingest (fc_ingest.cu) ---------------------------------------
+    def ingest(self, text: bytes, stages: int = 2) -> dict:
+        r = IngestResultC()
+        self._c(lib().fc_ingest_edge_list(self.h, text, len(text), stages, C.byref(r)))
+        edges = _take(r.edges, 2 * r.num_edges, np.uint32).reshape(-1, 2)
+        ids = _take(r.original_ids, r.num_nodes, np.int64)
+        return {"parsed_nodes": int(r.parsed_nodes), "lcc_nodes": int(r.lcc_nodes), "num_nodes": int(r.num_nodes),
+                "edges": edges, "original_ids": ids}
+
+    def _graph_nodes(self, fn, num_nodes, edges):
+        e = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+        out = _u32p()
+        cnt = C.c_uint64()
+        self._c(fn(self.h, int(num_nodes), e.shape[0], _p(e, _u32p), C.byref(out), C.byref(cnt)))
+        return _take(out, cnt.value, np.uint32)
+
+    def lcc_nodes(self, num_nodes, edges):
+        return self._graph_nodes(lib().fc_graph_lcc_nodes, num_nodes, edges)
+
+    def two_core_nodes(self, num_nodes, edges):
+        return self._graph_nodes(lib().fc_graph_two_core_nodes, num_nodes, edges)
 
     def cross_share(self, a, b):
         a = np.ascontiguousarray(a, dtype=np.float64)

@@ -237,6 +237,36 @@ TEST(SecondOrder, HessianVectorProductOnSevenNode) {
     EXPECT_DOUBLE_EQ(a(0, 1), a01);
 }
 
+TEST(Graph, ParseLccCoreLikeGraphTest) {
+    std::istringstream in("10 30\n30 20\n# comment\n\n20 10\n");
+    const auto p = parse_edge_list(in);
+    EXPECT_EQ(p.original_ids.size(), 3u);
+    EXPECT_EQ(p.original_ids[1], 30);
+    std::istringstream dup("0 1\n1 2\n2 0\n1 1\n0 1\n");
+    const auto g = parse_edge_list(dup).graph;
+    EXPECT_EQ(g.num_nodes, 3u);
+    EXPECT_EQ(g.edges.size(), 3u);
+    bool threw = false;
+    try {
+        std::istringstream bad("0 1\n1 2 3\n");
+        parse_edge_list(bad);
+    } catch (const IoError& e) {
+        threw = std::string(e.what()).find("line 2") != std::string::npos;
+    }
+    EXPECT_TRUE(threw);
+    Graph tie;
+    tie.num_nodes = 8;
+    tie.edges = {{0, 1}, {0, 2}, {1, 2}, {3, 4}, {4, 5}, {6, 7}};
+    const Graph lcc = largest_connected_component(tie);
+    EXPECT_EQ(lcc.num_nodes, 3u);
+    EXPECT_EQ(lcc.edges.size(), 3u);
+    Graph path;
+    path.num_nodes = 4;
+    path.edges = {{0, 1}, {1, 2}, {2, 3}};
+    EXPECT_EQ(prune_degree_one(path).num_nodes, 0u);
+    EXPECT_TRUE(is_connected(path));
+}
+
 int dump() {
     // seven_node goldens: name x0-kind seed method step max_iter restart trace_every
     struct Run { const char* name; InitKind k; std::uint64_t seed; Method m; double step; std::size_t it; bool rs; std::size_t te; };
