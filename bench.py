@@ -96,6 +96,11 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a moment to start: wait for its first sample so a short
+            # timed region still has one (taken as the region starts)
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -106,6 +111,10 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            n0 = len(self.lines)
+            t0 = time.time()
+            while len(self.lines) == n0 and time.time() - t0 < 0.3:   # one sample at the region's end
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
