@@ -308,11 +308,28 @@ def main():
     e2e = None
     if not args.no_e2e:
         ecfg = capi.Context.config(method=method, step_size=step0, max_iter=args.steps, fista_restart=True)
+        # page-locked host buffers (the contract's "pinned host memory"), filled before timing;
+        # the library DMAs page-locked buffers directly (pageable ones go through its staging ring)
+        keep = []
+
+        def pinned(a, view=None):
+            tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.float64): torch.float64,
+                   np.dtype(np.uint32): torch.int32}[a.dtype]
+            t = torch.empty(a.size, dtype=tdt, pin_memory=True)
+            keep.append(t)
+            arr = t.numpy().view(a.dtype).reshape(a.shape)
+            arr[...] = a
+            return arr
+
+        g_pin = fc.SparseSimilarity(graph.n, pinned(graph.row_ptr), pinned(graph.col_idx),
+                                    None if graph.values is None else pinned(graph.values), graph.frob_sq)
+        x0_pin = pinned(x0)
+        out_pin = pinned(np.zeros_like(x0))
         barrier(world)
         t0 = time.perf_counter()
-        ctx.upload(graph)                              # CSR H2D (shard)
+        ctx.upload(g_pin)                              # CSR H2D (shard)
         tu = time.perf_counter()
-        r = ctx.solve(x0, ecfg, want_x=True)           # x0 H2D, solve, membership + trace D2H
+        r = ctx.solve(x0_pin, ecfg, want_x=True, out=out_pin)   # x0 H2D, solve, membership + trace D2H
         t1 = time.perf_counter()
         e_local = t1 - t0
         e_s = allmax(e_local, world)
@@ -323,7 +340,8 @@ def main():
         e2e = {"value": r["iterations"] / e_s, "unit": "iter/s", "h2d_bytes_per_step": int(h2d / max(1, r["iterations"])),
                "d2h_bytes_per_step": int(d2h / max(1, r["iterations"])), "seconds": e_s,
                "iterations": r["iterations"], "upload_s": tu - t0, "solve_call_s": t1 - tu,
-               "includes": "CSR upload + x0 H2D + prelude + solve + result D2H"}
+               "includes": "CSR upload + x0 H2D + prelude + solve + result D2H",
+               "host_buffers": "page-locked (torch pin_memory), allocated and filled before the timed region"}
 
     # ---- roofline of the dominant kernel (k_sweep) -----------------------------------------
     peak, peak_kind = peaks()

@@ -368,13 +368,21 @@ class Context:
                bt_eta=2.0, bt_max=30):
         return SolverConfigC(step_size, max_iter, tol, method, int(fista_restart), trace_every, bt_eta, bt_max, 0)
 
-    def solve(self, x0, cfg: SolverConfigC, want_x: bool = True, trace_cap: int | None = None):
+    def solve(self, x0, cfg: SolverConfigC, want_x: bool = True, trace_cap: int | None = None, out=None):
+        """fc_solve.  `out`: optional preallocated (n, c) float64 result buffer (e.g. a
+        page-locked one, which the library fills by direct DMA)."""
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         n, c = x0.shape
         cap = trace_cap if trace_cap is not None else int(min(cfg.max_iter + 2, 1 << 20))
         recs = (TraceRecordC * max(cap, 1))()
         summ = SummaryC()
-        out = np.empty_like(x0) if want_x else None
+        if want_x:
+            if out is None:
+                out = np.empty_like(x0)
+            elif out.shape != x0.shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+                raise ValueError("solve: out must be a C-contiguous float64 array shaped like x0")
+        else:
+            out = None
         self._c(lib().fc_solve(self.h, C.byref(cfg), c, _p(x0), _p(out), recs, cap, C.byref(summ)))
         return _result(out, recs, summ, cap)
 

@@ -30,6 +30,9 @@
 #include <cstring>
 #include <string>
 #include <thread>
+#include <condition_variable>
+#include <mutex>
+#include <sys/mman.h>
 #include <unordered_map>
 #include <vector>
 
@@ -69,6 +72,22 @@ struct Shard {
 };
 
 enum { kClsStep, kClsGram, kClsSweep, kClsRowsum, kClsCombine, kClsFinalize, kClsComm, kNumCls };
+
+struct CopyPool {
+    std::vector<std::thread> th;
+    std::mutex mu;
+    std::condition_variable cv, done;
+    uint64_t gen = 0;
+    int pending = 0, nthreads = 1;
+    bool stop = false;
+    char* dst = nullptr;
+    const char* src = nullptr;
+    size_t bytes = 0;
+    void start(int n);
+    void run(int i);
+    void copy(void* d, const void* s, size_t b);
+    ~CopyPool();
+};
 
 }  // namespace
 
@@ -140,6 +159,7 @@ struct fc_ctx {
     char* stage_buf[kStageBufs] = {nullptr, nullptr, nullptr};
     cudaEvent_t stage_ev[kStageBufs] = {nullptr, nullptr, nullptr};
     int copy_threads = 8;
+    CopyPool pool;                     // persistent host-copy workers of the staging ring
 
     std::unordered_map<const void*, size_t> caps;   // device allocation capacities (bytes)
 
@@ -481,6 +501,13 @@ int set_hot_rows(fc_ctx* ctx) {
     double mb = 0.0;
     if (const char* e = std::getenv("FC_HOT_MB")) mb = std::atof(e);
     unsigned thr = 0xFFFFFFFFu;
+    if (mb > 0.0 && ctx->deg_hist.empty() && ctx->d_deg) {
+        std::vector<unsigned> deg(ctx->n);
+        CU(cudaMemcpy(deg.data(), ctx->d_deg, ctx->n * sizeof(unsigned), cudaMemcpyDeviceToHost));
+        const unsigned maxd = deg.empty() ? 0u : *std::max_element(deg.begin(), deg.end());
+        ctx->deg_hist.assign((size_t)maxd + 1, 0);
+        for (unsigned d : deg) ctx->deg_hist[d]++;
+    }
     if (mb > 0.0 && !ctx->deg_hist.empty()) {
         const double rows_budget = mb * 1e6 / (2.0 * 8.0 * ctx->c);
         uint64_t cum = 0;
@@ -779,21 +806,60 @@ int d2h(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
 // Pageable cudaMemcpy moves data through one driver thread; here the host side
 // of each 64 MB chunk is copied by several threads into pinned memory while the
 // previous chunk's DMA runs.
-void par_memcpy(void* dst, const void* src, size_t bytes, int threads) {
-    if (threads <= 1 || bytes < (size_t(4) << 20)) {
-        std::memcpy(dst, src, bytes);
+// Host copies of the staging ring through persistent workers (spawning threads per
+// 64 MB chunk cost ~10% of a multi-GB transfer).  The caller takes part 0.
+void CopyPool::start(int n) {
+    if (!th.empty() || n <= 1) return;
+    nthreads = n;
+    for (int i = 1; i < n; ++i) th.emplace_back([this, i] { run(i); });
+}
+void CopyPool::run(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+        char* d = dst;
+        const char* s2 = src;
+        const size_t b = bytes, part = (bytes + nthreads - 1) / nthreads;
+        lk.unlock();
+        const size_t a = std::min(b, (size_t)i * part), e = std::min(b, a + part);
+        if (e > a) std::memcpy(d + a, s2 + a, e - a);
+        lk.lock();
+        if (--pending == 0) done.notify_one();
+    }
+}
+void CopyPool::copy(void* d, const void* s2, size_t b) {
+    if (th.empty() || b < (size_t(4) << 20)) {
+        std::memcpy(d, s2, b);
         return;
     }
-    std::vector<std::thread> pool;
-    const size_t part = (bytes + threads - 1) / threads;
-    for (int t = 0; t < threads; ++t) {
-        const size_t a = std::min(bytes, (size_t)t * part), b = std::min(bytes, a + part);
-        if (b > a) pool.emplace_back([=] { std::memcpy((char*)dst + a, (const char*)src + a, b - a); });
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        dst = (char*)d;
+        src = (const char*)s2;
+        bytes = b;
+        pending = nthreads - 1;
+        ++gen;
     }
-    for (auto& th : pool) th.join();
+    cv.notify_all();
+    const size_t part = (b + nthreads - 1) / nthreads;
+    std::memcpy(d, s2, std::min(b, part));
+    std::unique_lock<std::mutex> lk(mu);
+    done.wait(lk, [&] { return pending == 0; });
+}
+CopyPool::~CopyPool() {
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
 }
 
 int ensure_staging(fc_ctx* ctx) {
+    ctx->pool.start(ctx->copy_threads);
     for (int k = 0; k < fc_ctx::kStageBufs; ++k) {
         if (!ctx->stage_buf[k]) CU(cudaMallocHost(reinterpret_cast<void**>(&ctx->stage_buf[k]), fc_ctx::kStageChunk));
         if (!ctx->stage_ev[k]) CU(cudaEventCreateWithFlags(&ctx->stage_ev[k], cudaEventDisableTiming));
@@ -801,24 +867,54 @@ int ensure_staging(fc_ctx* ctx) {
     return FC_OK;
 }
 
+// Page-locked (cudaHostAlloc / registered / torch pin_memory) host memory is DMA'd
+// directly at full link speed; pageable memory goes through the staging ring.
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 // Returns once `src` has been consumed (the DMA may still be in flight, stream-ordered).
 int h2d_big(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
     if (bytes < (size_t(8) << 20)) return h2d(ctx, dst, src, bytes);
+    if (host_pinned(src)) {
+        CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        return FC_OK;
+    }
     TRY(ensure_staging(ctx));
     const size_t ch = fc_ctx::kStageChunk;
     int k = 0;
     for (size_t off = 0; off < bytes; off += ch, k = (k + 1) % fc_ctx::kStageBufs) {
         const size_t n = std::min(ch, bytes - off);
         CU(cudaEventSynchronize(ctx->stage_ev[k]));           // buffer k's previous DMA has finished
-        par_memcpy(ctx->stage_buf[k], (const char*)src + off, n, ctx->copy_threads);
+        ctx->pool.copy(ctx->stage_buf[k], (const char*)src + off, n);
         CU(cudaMemcpyAsync((char*)dst + off, ctx->stage_buf[k], n, cudaMemcpyHostToDevice, ctx->stream));
         CU(cudaEventRecord(ctx->stage_ev[k], ctx->stream));
     }
     return FC_OK;
 }
 
+// Large, freshly allocated destinations fault in 4 KB pages as the copy threads touch
+// them (~0.1 s for 2.5 GB); ask for transparent huge pages on the aligned interior.
+void advise_huge(void* p, size_t bytes) {
+    const uintptr_t a = ((uintptr_t)p + (size_t(2) << 20) - 1) & ~((uintptr_t(2) << 20) - 1);
+    const uintptr_t b = ((uintptr_t)p + bytes) & ~((uintptr_t(2) << 20) - 1);
+    if (b > a) madvise((void*)a, b - a, MADV_HUGEPAGE);
+}
+
 // Synchronous: `dst` holds the data on return.
 int d2h_big(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes >= (size_t(8) << 20) && host_pinned(dst)) {
+        CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        return FC_OK;
+    }
+    if (bytes >= (size_t(64) << 20)) advise_huge(dst, bytes);
     if (bytes < (size_t(8) << 20)) {
         TRY(d2h(ctx, dst, src, bytes));
         CU(cudaStreamSynchronize(ctx->stream));
@@ -839,7 +935,7 @@ int d2h_big(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
         const int k = (int)(i % fc_ctx::kStageBufs);
         const size_t off = i * ch, n = std::min(ch, bytes - off);
         CU(cudaEventSynchronize(ctx->stage_ev[k]));
-        par_memcpy((char*)dst + off, ctx->stage_buf[k], n, ctx->copy_threads);
+        ctx->pool.copy((char*)dst + off, ctx->stage_buf[k], n);
         if (i + fc_ctx::kStageBufs < nchunks) TRY(issue(i + fc_ctx::kStageBufs));
     }
     return FC_OK;
@@ -1086,10 +1182,15 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
     if (weighted) TRY(dalloc(ctx, &ctx->d_val, lnnz));
     else dfree(ctx, &ctx->d_val);
     {
-        std::vector<long long> rp(lrow + 1);
-        for (uint64_t i = 0; i <= lrow; ++i) rp[i] = (long long)(row_ptr[r0 + i] - e0);
-        TRY(h2d_big(ctx, ctx->d_row_ptr, rp.data(), rp.size() * sizeof(long long)));
-        CU(cudaStreamSynchronize(ctx->stream));
+        HostPhase hp("row_ptr");
+        if (e0 == 0) {                                       // this device's slice starts at entry 0
+            TRY(h2d_big(ctx, ctx->d_row_ptr, row_ptr + r0, (lrow + 1) * sizeof(long long)));
+        } else {
+            std::vector<long long> rp(lrow + 1);
+            for (uint64_t i = 0; i <= lrow; ++i) rp[i] = (long long)(row_ptr[r0 + i] - e0);
+            TRY(h2d_big(ctx, ctx->d_row_ptr, rp.data(), rp.size() * sizeof(long long)));
+            CU(cudaStreamSynchronize(ctx->stream));
+        }
     }
     if (src_device) {
         CU(cudaMemcpyAsync(ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1106,16 +1207,18 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
     // node degrees (== column counts, S symmetric) for the hot-row L2 policy
     {
         HostPhase hp("degrees");
-        std::vector<unsigned> deg(n);
-        uint64_t maxd = 0;
-        for (uint64_t i = 0; i < n; ++i) {
-            deg[i] = (unsigned)std::min<int64_t>(row_ptr[i + 1] - row_ptr[i], 0xFFFFFFFELL);
-            maxd = std::max<uint64_t>(maxd, deg[i]);
-        }
-        ctx->deg_hist.assign(maxd + 1, 0);
-        for (uint64_t i = 0; i < n; ++i) ctx->deg_hist[deg[i]]++;
         TRY(dalloc(ctx, &ctx->d_deg, n));
-        CU(cudaMemcpy(ctx->d_deg, deg.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice));
+        ctx->deg_hist.clear();                               // built on demand (set_hot_rows)
+        if (ctx->world == 1) {                               // local rows == all rows: from the device CSR
+            k_degrees<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(ctx->d_row_ptr, n, ctx->d_deg);
+            TRY(check_launch(ctx, "k_degrees"));
+        } else {
+            std::vector<unsigned> hdeg(n);
+            for (uint64_t i = 0; i < n; ++i)
+                hdeg[i] = (unsigned)std::min<int64_t>(row_ptr[i + 1] - row_ptr[i], 0xFFFFFFFELL);
+            CU(cudaMemcpy(ctx->d_deg, hdeg.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice));
+        }
+        auto deg = [&](uint64_t i) { return (uint64_t)(row_ptr[i + 1] - row_ptr[i]); };
         // heavy rows per shard (k_sweep phase 1), longest first
         std::vector<unsigned> heavy;
         ctx->heavy_off.assign(ctx->shards.size(), 0);
@@ -1124,9 +1227,9 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
             const Shard& S = ctx->shards[sh];
             const size_t first = heavy.size();
             for (uint64_t i = S.row0; i < S.row0 + S.nrows; ++i)
-                if (deg[i] >= ctx->heavy_deg) heavy.push_back((unsigned)(i - S.row0));
+                if (deg(i) >= ctx->heavy_deg) heavy.push_back((unsigned)(i - S.row0));
             std::stable_sort(heavy.begin() + first, heavy.end(),
-                             [&](unsigned a, unsigned b2) { return deg[S.row0 + a] > deg[S.row0 + b2]; });
+                             [&](unsigned a, unsigned b2) { return deg(S.row0 + a) > deg(S.row0 + b2); });
             ctx->heavy_off[sh] = first;
             ctx->heavy_cnt[sh] = heavy.size() - first;
         }
@@ -1139,14 +1242,13 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
     }
     ctx->local_nnz = lnnz;
     {   // fingerprint of the shard CSR (checked by fc_solver_resume); before hot flags are set
-        unsigned long long* d_fp = nullptr;
-        CU(cudaMallocAsync(&d_fp, sizeof(unsigned long long), ctx->stream));
+        HostPhase hp("fingerprint+sync");
+        unsigned long long* d_fp = reinterpret_cast<unsigned long long*>(ctx->d_counter + 96);
         CU(cudaMemsetAsync(d_fp, 0, sizeof(unsigned long long), ctx->stream));
         k_fingerprint<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(ctx->d_row_ptr, lrow, ctx->d_col,
                                                                    weighted ? ctx->d_val : nullptr, lnnz, d_fp);
         TRY(check_launch(ctx, "k_fingerprint"));
         CU(cudaMemcpyAsync(&ctx->csr_fp, d_fp, sizeof ctx->csr_fp, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaFreeAsync(d_fp, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
     }
     ctx->hot_threshold = 0xFFFFFFFFu;

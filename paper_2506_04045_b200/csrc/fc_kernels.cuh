@@ -1501,23 +1501,28 @@ __global__ void k_hvp_rows(const double* g2, const double* vs, const double* x, 
     }
 }
 
-// Fingerprint of the resident CSR (checkpoint compatibility): sum over entries of
-// a mix of (position, column, value bits), order-sensitive through the position.
-__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
+__global__ void k_degrees(const long long* row_ptr, unsigned long long n, unsigned* deg) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const long long d = row_ptr[i + 1] - row_ptr[i];
+        deg[i] = (unsigned)(d < 0xFFFFFFFELL ? d : 0xFFFFFFFELL);
+    }
 }
+
+// Fingerprint of the resident CSR (checkpoint compatibility, not cryptographic):
+// sum over entries of (column + 1) * (2 * position + 1) (+ the value bits when
+// weighted) and of row_ptr[r] * (2r + 1) -- order-sensitive, one 64-bit multiply each.
 __global__ void k_fingerprint(const long long* row_ptr, unsigned long long rows, const unsigned* col,
                               const double* val, unsigned long long nnz, unsigned long long* out) {
     unsigned long long acc = 0;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < nnz; k += stride) {
-        unsigned long long v = val ? (unsigned long long)__double_as_longlong(val[k]) : 0x3FF0000000000000ULL;
-        acc += mix64(k * 0x9E3779B97F4A7C15ULL ^ ((unsigned long long)(col[k] & kIdxMask) << 1) ^ mix64(v));
+        unsigned long long h = (unsigned long long)((col[k] & kIdxMask) + 1u);
+        if (val) h ^= (unsigned long long)__double_as_longlong(val[k]);
+        acc += h * (2ULL * k + 1ULL);
     }
     for (unsigned long long r = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; r <= rows; r += stride)
-        acc += mix64(~(r * 0xD1B54A32D192ED03ULL) ^ (unsigned long long)row_ptr[r]);
+        acc += (unsigned long long)row_ptr[r] * (0x9E3779B97F4A7C15ULL ^ (2ULL * r + 1ULL));
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
