@@ -292,7 +292,7 @@ template <int G, int S, bool DUAL, bool W, bool EXACT>
 int launch_sweep_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     static int grid = 0;
     if (!grid) grid = grid_for((const void*)k_sweep<G, S, DUAL, W, EXACT>, 256, 0, ctx->sm_count);
-    const unsigned long long need = (g.nrows + 31) / 32;   // 32-row chunks, 8 warps per CTA
+    const unsigned long long need = (g.nrows + g.chunk - 1) / g.chunk;   // row chunks, 8 warps per CTA
     const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, (need + 7) / 8));
     k_sweep<G, S, DUAL, W, EXACT><<<gr, 256, 0, ctx->stream>>>(b, g);
     ctx->launches++;
@@ -324,7 +324,7 @@ template <int G, bool DUAL, bool W>
 int launch_sweep_small(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     static int grid = 0;
     if (!grid) grid = grid_for((const void*)k_sweep_small<G, DUAL, W>, 256, 0, ctx->sm_count);
-    const unsigned long long need = (g.nrows + 31) / 32;
+    const unsigned long long need = (g.nrows + g.chunk - 1) / g.chunk;
     const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, (need + 7) / 8));
     k_sweep_small<G, DUAL, W><<<gr, 256, 0, ctx->stream>>>(b, g);
     ctx->launches++;
@@ -597,6 +597,8 @@ Geo make_geo(fc_ctx* ctx, size_t s) {
     g.nrows = sh.nrows;
     g.nblk = sh.nblk;
     g.spart_stride = ctx->local_blocks;
+    // enough counter grabs to occupy every resident warp (~32 per SM) when N is small
+    g.chunk = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(32, sh.nrows / ((uint64_t)ctx->sm_count * 32)));
     return g;
 }
 
@@ -621,17 +623,18 @@ int phase_step(fc_ctx* ctx, int bt) {
 int phase_gram(fc_ctx* ctx, bool dual) {
     ProfScope p(ctx, kClsGram);
     const uint32_t c = ctx->c;
-    const int c4 = (int)((c + 3) & ~3u);
-    const int nT = c4 / 4;
+    // few 1024-row blocks (small N): one thread per (r, s) pair, larger chunks (fewer barriers)
+    const bool few = ctx->local_blocks < (uint64_t)ctx->sm_count * 2;
+    const int TS = few ? 1 : 4;
+    const int nT = ((int)c + TS - 1) / TS;
     const int tiles = nT * (nT + 1) / 2 * (dual ? 2 : 1);
     int R = gram_rows_per_chunk(c);
-    // few blocks (small N): occupancy is no concern, larger chunks mean fewer barriers
-    if (ctx->local_blocks < (uint64_t)ctx->sm_count * 2) R = std::max(R, std::min(128, 4096 / (int)((c + 3) & ~3u)));
+    if (few) R = std::max(R, std::min(128, 4096 / (int)((c + 3) & ~3u)));
     const size_t smem = gram_smem((int)c, dual ? 1 : 0, R);
-    static size_t smem_set = 0;
-    if (smem > 48 * 1024 && smem > smem_set) {
-        CU(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = smem;
+    static size_t smem_set[2] = {0, 0};
+    if (smem > 48 * 1024 && smem > smem_set[few]) {
+        CU(cudaFuncSetAttribute(few ? k_gram<1> : k_gram<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set[few] = smem;
     }
     for (size_t s = 0; s < ctx->shards.size(); ++s) {
         const Geo g = make_geo(ctx, s);
@@ -639,7 +642,8 @@ int phase_gram(fc_ctx* ctx, bool dual) {
         const Bufs b = make_bufs(ctx, s);
         const int threads = std::min(kGramMaxThreads, (tiles + 31) / 32 * 32);
         dim3 grid((unsigned)g.nblk, (unsigned)((tiles + threads - 1) / threads));
-        k_gram<<<grid, threads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
+        if (few) k_gram<1><<<grid, threads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
+        else k_gram<4><<<grid, threads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
         TRY(check_launch(ctx, "k_gram"));
     }
     return FC_OK;

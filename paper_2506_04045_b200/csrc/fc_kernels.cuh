@@ -119,6 +119,7 @@ struct Geo {
     unsigned long long nrows;
     unsigned long long nblk;        // blocks of the shard
     unsigned long long spart_stride;
+    unsigned chunk;                 // k_sweep rows per scheduler grab: 32, fewer when N is small
 };
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -448,7 +449,7 @@ template <int G, int S, bool DUAL, bool W, bool EXACT>
 __global__ void __launch_bounds__(256, SweepTune<G, S>::MINB) k_sweep(Bufs b, Geo g) {
     const DevState* st = b.st;
     if (st->done) return;
-    constexpr unsigned kChunk = 32;
+    const unsigned kChunk = g.chunk;                        // rows per counter grab (<= 32)
     const unsigned C = g.C;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned lg = lane % G;
@@ -786,7 +787,7 @@ template <int G, bool DUAL, bool W>
 __global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
     const DevState* st = b.st;
     if (st->done) return;
-    constexpr unsigned kChunk = 32;
+    const unsigned kChunk = g.chunk;                        // rows per counter grab (<= 32)
     constexpr int Q = 32 / G;                 // nonzeros per load instruction
     constexpr int U = (32 / Q) < 8 ? (32 / Q) : 8;  // loads per lane in flight per batch (x2 DUAL)
     const unsigned C = g.C;
@@ -964,13 +965,17 @@ __host__ __device__ inline size_t gram_smem(int C, int dual, int R) {
     return sizeof(double) * (size_t)R * C4 * (dual ? 5 : 2);
 }
 
+// TS x TS register tiles: TS = 4 in general; TS = 1 when there are few 1024-row
+// blocks (small N): every (r, s) pair gets its own thread, so the 1024-long
+// sequential chains of all pairs run in parallel instead of 16 per thread.
+template <int TS>
 __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dual, int rows_per_chunk) {
     const DevState* st = b.st;
     if (st->done) return;
     extern __shared__ double smg[];
     const int C = (int)g.C;
     const int C4 = (C + 3) & ~3;
-    const int nT = C4 / 4;
+    const int nT = (C + TS - 1) / TS;
     const int tiles_per_mat = nT * (nT + 1) / 2;
     const int nmat = dual ? 2 : 1;
     const int tile = blockIdx.y * blockDim.x + threadIdx.x;
@@ -1010,11 +1015,11 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
         cp_async_commit();
     };
 
-    double acc[4][4];
+    double acc[TS][TS];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < TS; ++a)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+        for (int c = 0; c < TS; ++c) acc[a][c] = 0.0;
 
     issue(0, r0);
     int sidx = 0;
@@ -1036,15 +1041,24 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
         if (has) {
             const double* t = mat_local == 0 ? tb : te;
             for (int rr = 0; rr < rows; ++rr) {
-                const double2* rowp = reinterpret_cast<const double2*>(t + rr * C4);
-                const double2 r01 = rowp[2 * I], r23 = rowp[2 * I + 1];
-                const double2 q01 = rowp[2 * J], q23 = rowp[2 * J + 1];
-                const double xr[4] = {r01.x, r01.y, r23.x, r23.y};
-                const double xq[4] = {q01.x, q01.y, q23.x, q23.y};
+                double xr[TS], xq[TS];
+                if constexpr (TS == 4) {
+                    const double2* rowp = reinterpret_cast<const double2*>(t + rr * C4);
+                    const double2 r01 = rowp[2 * I], r23 = rowp[2 * I + 1];
+                    const double2 q01 = rowp[2 * J], q23 = rowp[2 * J + 1];
+                    xr[0] = r01.x; xr[1] = r01.y; xr[2] = r23.x; xr[3] = r23.y;
+                    xq[0] = q01.x; xq[1] = q01.y; xq[2] = q23.x; xq[3] = q23.y;
+                } else {
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < TS; ++a) {
+                        xr[a] = t[rr * C4 + TS * I + a];
+                        xq[a] = t[rr * C4 + TS * J + a];
+                    }
+                }
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[a][c] = dadd(acc[a][c], dmul(xr[a], xq[c]));
+                for (int a = 0; a < TS; ++a)
+#pragma unroll
+                    for (int c = 0; c < TS; ++c) acc[a][c] = dadd(acc[a][c], dmul(xr[a], xq[c]));
             }
         }
         __syncthreads();                                     // stage sidx is re-filled next round
@@ -1052,10 +1066,10 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
     if (has) {
         double* out = b.gpart[out_mat] + (size_t)blk * g.npairs;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < TS; ++a)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int r = 4 * I + a, s = 4 * J + c;
+            for (int c = 0; c < TS; ++c) {
+                const int r = TS * I + a, s = TS * J + c;
                 if (r <= s && s < C) out[pair_index(r, s, C)] = acc[a][c];
             }
     }
