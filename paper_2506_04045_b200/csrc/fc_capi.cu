@@ -160,6 +160,11 @@ struct fc_ctx {
     cudaEvent_t stage_ev[kStageBufs] = {nullptr, nullptr, nullptr};
     int copy_threads = 8;
     CopyPool pool;                     // persistent host-copy workers of the staging ring
+    // one captured iteration (CUDA graph), replayed while the key (every kernel argument) matches
+    cudaGraphExec_t iter_exec = nullptr;
+    std::vector<char> iter_key;
+    uint64_t iter_launches = 0;
+    bool graphs = true;                // FC_GRAPHS=0 disables
 
     std::unordered_map<const void*, size_t> caps;   // device allocation capacities (bytes)
 
@@ -1034,6 +1039,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         ctx->sweep_groups = std::strcmp(sw, "groups") == 0;
     }
     if (const char* sp = std::getenv("FC_STEP")) ctx->step_big = std::strcmp(sp, "big") == 0;
+    if (const char* gr = std::getenv("FC_GRAPHS")) ctx->graphs = std::strcmp(gr, "0") != 0;
     {
         const unsigned hw = std::thread::hardware_concurrency();
         ctx->copy_threads = (int)std::max(1u, std::min(8u, hw ? hw / 2 : 1u));
@@ -1088,6 +1094,7 @@ void fc_destroy(fc_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     prof_harvest(ctx);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->iter_exec) cudaGraphExecDestroy(ctx->iter_exec);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     for (int k = 0; k < 3; ++k) dfree(ctx, &ctx->d_U[k]);
     for (int k = 0; k < 4; ++k) dfree(ctx, &ctx->d_xs[k]);
@@ -1557,12 +1564,68 @@ int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const 
     return FC_OK;
 }
 
+static int enqueue_iteration(fc_ctx* ctx) {
+    if (ctx->method == FC_GPA) return enqueue_gpa_iteration(ctx);
+    return enqueue_fista_iteration(ctx, ctx->method == FC_FISTA_BT);
+}
+
+// Key of a captured iteration: everything its kernels take by value.
+static std::vector<char> iteration_key(fc_ctx* ctx) {
+    std::vector<char> k;
+    auto put = [&](const void* p, size_t n) { k.insert(k.end(), (const char*)p, (const char*)p + n); };
+    put(&ctx->method, sizeof ctx->method);
+    put(&ctx->c, sizeof ctx->c);
+    for (size_t s = 0; s < ctx->shards.size(); ++s) {
+        const Bufs b = make_bufs(ctx, s);
+        const Geo g = make_geo(ctx, s);
+        put(&b, sizeof b);
+        put(&g, sizeof g);
+    }
+    const Bufs fb = final_bufs(ctx);
+    put(&fb, sizeof fb);
+    return k;
+}
+
+// One iteration as a CUDA graph replay (the plan lives in DevState, so every
+// iteration of a session enqueues the same kernels with the same arguments):
+// removes the per-kernel launch gaps that dominate small-N iterations.
+static int launch_iteration(fc_ctx* ctx) {
+    if (!ctx->graphs || ctx->comm || ctx->profiling) return enqueue_iteration(ctx);
+    std::vector<char> key = iteration_key(ctx);
+    if (!ctx->iter_exec || key != ctx->iter_key) {
+        if (ctx->iter_exec) {
+            cudaGraphExecDestroy(ctx->iter_exec);
+            ctx->iter_exec = nullptr;
+        }
+        const uint64_t l0 = ctx->launches;
+        CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+        const int rc = enqueue_iteration(ctx);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &graph);
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (ec != cudaSuccess) return set_err(ctx, FC_DEVICE, "iteration capture: %s", cudaGetErrorString(ec));
+        const cudaError_t ei = cudaGraphInstantiate(&ctx->iter_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ei != cudaSuccess) return set_err(ctx, FC_DEVICE, "iteration graph: %s", cudaGetErrorString(ei));
+        ctx->iter_launches = ctx->launches - l0;
+        ctx->launches -= ctx->iter_launches;      // counted per replay below
+        ctx->iter_key = std::move(key);
+    } else {
+        ctx->host_iter++;                            // what enqueue_iteration would have advanced
+    }
+    CU(cudaGraphLaunch(ctx->iter_exec, ctx->stream));
+    ctx->launches += ctx->iter_launches;
+    return FC_OK;
+}
+
 int fc_solver_run(fc_ctx* ctx, uint64_t iterations) {
     if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
     CU(cudaSetDevice(ctx->device));
     for (uint64_t k = 0; k < iterations; ++k) {
-        if (ctx->method == FC_GPA) TRY(enqueue_gpa_iteration(ctx));
-        else TRY(enqueue_fista_iteration(ctx, ctx->method == FC_FISTA_BT));
+        TRY(launch_iteration(ctx));
         ctx->enqueued++;
     }
     return FC_OK;
