@@ -108,6 +108,26 @@ int fc_cross_share(fc_ctx* ctx, uint32_t c, const double* a, const double* b, do
  * similarity: out_i = -4 (V s_i - A x_i - A^T x_i - B v_i), A = cross_share(V, X),
  * B = share_matrix(X); x, v, out n x c node-major; c <= 128. */
 int fc_hessian_vector_product(fc_ctx* ctx, uint32_t c, const double* x, const double* v, double* out);
+/* The pairwise part of refine (secondorder.hpp:132-330) for a critical point x with
+ * gradient grad (both n x c node-major): the kept pair directions V = e_k - e_l at
+ * node i (critical_cone_directions' filter and order) are enumerated and evaluated
+ * on the device without materialising them; condition (a) <H V, V> (bit-identical
+ * to quadratic_form) and condition (b) <grad, W> over the W each V admits, both over
+ * the first `budget` directions, ties to the first in enumeration order.
+ * triples_out (optional, 3 * min(pairs, triples_cap)): (node, plus, minus) per pair. */
+typedef struct fc_refine_pairs_out {
+    uint64_t pairs;                            /* kept pair directions */
+    double a_worst;                            /* min(0, min <H V, V>) */
+    uint64_t a_index;                          /* its direction index (UINT64_MAX: none < 0) */
+    uint32_t a_col, a_plus, a_minus, pad0;     /* that direction: node, +1 row, -1 row */
+    double b_worst;                            /* min(0, min <grad, W>) */
+    uint64_t b_index;                          /* index of the base direction V (UINT64_MAX: none) */
+    uint32_t b_col, b_plus, b_minus;           /* W = e_plus - e_minus at node b_col */
+    uint32_t b_base_plus, b_base_minus, pad1;  /* V = e_base_plus - e_base_minus at b_col */
+} fc_refine_pairs_out;
+int fc_refine_pairs(fc_ctx* ctx, uint32_t c, const double* x, const double* grad, double eps_active,
+                    double eps_grad_orth, uint64_t budget, uint32_t* triples_out, uint64_t triples_cap,
+                    fc_refine_pairs_out* out);
 /* frob_inner (dense.hpp:40-46) on the host: sum_k a[k] * b[k], strictly sequential
  * (quadratic_form = frob_inner(HVP, V)). */
 double fc_frob_inner(const double* a, const double* b, uint64_t count);

@@ -251,6 +251,10 @@ class Reference:
         L.fcref_graph_nodes.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint32), C.c_int,
                                         C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64)]
         L.fcref_free_buf.argtypes = [C.c_void_p]
+        L.fcref_refine.argtypes = [C.c_void_p, _dp, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double,
+                                   C.c_double, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64,
+                                   C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_uint64), C.POINTER(_RVerdict), C.POINTER(_RVerdict), _dp, _dp, _dp]
         L.fcref_cross_share.argtypes = [_dp, _dp, C.c_uint64, C.c_uint64, C.c_uint, _dp]
         L.fcref_hessian_vector_product.argtypes = [C.c_void_p, _dp, _dp, C.c_uint64, C.c_uint, _dp, _dp]
         L.fcref_gpa_step_fused.argtypes = [_dp, C.c_uint64, C.c_uint64, _dp, _dp, C.c_double, C.c_uint, _dp]
@@ -341,6 +345,11 @@ class Reference:
         return self.lib.fcref_fista_t_next(t)
 
 
+class _RVerdict(C.Structure):
+    _fields_ = [("status", C.c_int), ("has_witness", C.c_int), ("has_base", C.c_int),
+                ("interior_shortcut", C.c_int), ("tested", C.c_uint64), ("value", C.c_double)]
+
+
 class RefSimilarity:
     def __init__(self, ref: Reference, h):
         self.ref, self.h = ref, h
@@ -377,6 +386,25 @@ class RefSimilarity:
         self.ref._check(self.ref.lib.fcref_fused_column_pass(self.h, _ptr(x), x.shape[1], workers, _ptr(xs),
                                                              C.byref(m)))
         return xs, m.value
+
+    def refine(self, x, tau_probe=1e-2, eps_critical=1e-2, eps_active=1e-8, eps_grad_orth=1e-6, eps_quad=1e-8,
+               eps_cone=1e-9, random_directions=0, seed=0, budget=2**64 - 1):
+        """secondorder.hpp refine() of the reference: a dict of the report, dense witnesses."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        crit, st = C.c_int(), C.c_int()
+        res = C.c_double()
+        gen = C.c_uint64()
+        a, b = _RVerdict(), _RVerdict()
+        wa, wb, wbase = np.zeros_like(x), np.zeros_like(x), np.zeros_like(x)
+        self.ref._check(self.ref.lib.fcref_refine(
+            self.h, _ptr(x), x.shape[1], tau_probe, eps_critical, eps_active, eps_grad_orth, eps_quad, eps_cone,
+            random_directions, seed, budget, C.byref(crit), C.byref(res), C.byref(st), C.byref(gen), C.byref(a),
+            C.byref(b), _ptr(wa), _ptr(wb), _ptr(wbase)))
+        ver = lambda v, w, base: {"status": v.status, "tested": v.tested, "value": v.value,
+                                  "interior_shortcut": bool(v.interior_shortcut),
+                                  "witness": w if v.has_witness else None, "base": base if v.has_base else None}
+        return {"critical": bool(crit.value), "residual": res.value, "status": st.value,
+                "directions_generated": gen.value, "a": ver(a, wa, None), "b": ver(b, wb, wbase)}
 
     def hessian_vector_product(self, x, v, workers=1):
         """(HVP, quadratic_form) of the reference (objective.hpp:186-223)."""

@@ -283,6 +283,55 @@ int fcref_graph_nodes(uint64_t n, uint64_t m, const uint32_t* edges, int which, 
 
 void fcref_free_buf(void* p) { std::free(p); }
 
+struct fcref_verdict {
+    int status;
+    int has_witness;
+    int has_base;
+    int interior_shortcut;
+    uint64_t tested;
+    double value;
+};
+// secondorder.hpp:343-368 refine on the reference; dense witnesses copied out (n x c node-major)
+int fcref_refine(void* h, const double* x, uint64_t c, double tau_probe, double eps_critical, double eps_active,
+                 double eps_grad_orth, double eps_quad, double eps_cone, uint64_t random_directions, uint64_t seed,
+                 uint64_t budget, int* critical, double* residual, int* status, uint64_t* generated,
+                 fcref_verdict* a, fcref_verdict* b, double* a_witness, double* b_witness, double* b_base) {
+    return guarded([&] {
+        const auto& s = *static_cast<SparseSimilarity*>(h);
+        const auto m = wrap(x, c, s.size());
+        SecondOrderConfig cfg;
+        cfg.tau_probe = tau_probe;
+        cfg.eps_critical = eps_critical;
+        cfg.eps_active = eps_active;
+        cfg.eps_grad_orth = eps_grad_orth;
+        cfg.eps_quad = eps_quad;
+        cfg.eps_cone = eps_cone;
+        cfg.random_directions = random_directions;
+        cfg.seed = seed;
+        cfg.budget = budget;
+        const RefinementReport r = refine(m, s, cfg);
+        *critical = r.critical ? 1 : 0;
+        *residual = r.residual;
+        *status = static_cast<int>(r.status);
+        *generated = r.directions_generated;
+        auto fill = [&](const RefinementVerdict& v, fcref_verdict* o, double* w, double* base) {
+            o->status = static_cast<int>(v.status);
+            o->tested = v.directions_tested;
+            o->value = v.witness_value;
+            o->interior_shortcut = v.used_interior_shortcut ? 1 : 0;
+            o->has_witness = v.witness.has_value() ? 1 : 0;
+            o->has_base = v.witness_base.has_value() ? 1 : 0;
+            if (v.witness && w) std::memcpy(w, v.witness->data().data(), v.witness->data().size() * sizeof(double));
+            if (v.witness_base && base)
+                std::memcpy(base, v.witness_base->data().data(), v.witness_base->data().size() * sizeof(double));
+        };
+        fill(r.condition_a, a, a_witness, nullptr);
+        fill(r.condition_b, b, b_witness, b_base);
+    });
+}
+
+
+
 int fcref_loss_decomposed(void* h, const double* x, uint64_t c, unsigned workers, double* loss) {
     return guarded([&] {
         const auto& s = *static_cast<SparseSimilarity*>(h);

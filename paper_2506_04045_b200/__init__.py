@@ -19,4 +19,6 @@ from .api import (
     cross_share, hessian_vector_product, quadratic_form, frob_inner,
     Graph, ParsedGraph, LoadedGraph, parse_edge_list, largest_connected_component_nodes, two_core_nodes,
     induced_subgraph, largest_connected_component, prune_degree_one, load_pipeline, write_edge_list,
+    SecondOrderConfig, RefinementStatus, RefinementVerdict, RefinementReport, full_gradient, projection_residual,
+    is_critical, is_interior, refine,
 )

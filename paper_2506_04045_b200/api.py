@@ -417,6 +417,244 @@ def quadratic_form(xbar: np.ndarray, v: np.ndarray, s: SparseSimilarity, workers
     return frob_inner(hessian_vector_product(xbar, v, s, workers, ctx), v)
 
 
+# ---- secondorder.hpp refinement ------------------------------------
+@dataclass
+class SecondOrderConfig:             # secondorder.hpp:25-36
+    tau_probe: float = 1e-2
+    eps_critical: float = 1e-2
+    eps_active: float = 1e-8
+    eps_grad_orth: float = 1e-6
+    eps_quad: float = 1e-8
+    eps_cone: float = 1e-9
+    random_directions: int = 0
+    seed: int = 0
+    budget: int = 2**64 - 1
+    workers: int = 1
+
+
+class RefinementStatus(IntEnum):     # secondorder.hpp:195-200
+    kRefutedFirstOrder = 0
+    kRefutedConditionA = 1
+    kRefutedConditionB = 2
+    kSurviving = 3
+
+
+@dataclass
+class RefinementVerdict:             # secondorder.hpp:214-222; witnesses as {(node, row): value}
+    status: RefinementStatus = RefinementStatus.kSurviving
+    witness: dict | None = None
+    witness_base: dict | None = None
+    witness_value: float = 0.0
+    directions_tested: int = 0
+    used_interior_shortcut: bool = False
+
+
+@dataclass
+class RefinementReport:              # secondorder.hpp:333-340
+    critical: bool = False
+    residual: float = 0.0
+    status: RefinementStatus = RefinementStatus.kSurviving
+    condition_a: RefinementVerdict = field(default_factory=RefinementVerdict)
+    condition_b: RefinementVerdict = field(default_factory=RefinementVerdict)
+    directions_generated: int = 0
+
+
+def full_gradient(x: np.ndarray, s: SparseSimilarity, ctx: capi.Context | None = None) -> np.ndarray:
+    """secondorder.hpp:39-52: -4 (X S - (X X^T) X) column by column, on the device."""
+    c = _ctx_for(s, ctx)
+    share = c.share_matrix(x)
+    xs, _ = c.fused_column_pass(x)
+    return c.gradient_rows(share, xs, x)
+
+
+def projection_residual(x: np.ndarray, s: SparseSimilarity, tau_probe: float,
+                        ctx: capi.Context | None = None) -> float:
+    """secondorder.hpp:56-68: ||P(X - tau grad) - X||_F (sum sequential in storage order)."""
+    c = _ctx_for(s, ctx)
+    d = c.gpa_step(x, c.share_matrix(x), tau_probe) - np.asarray(x, dtype=np.float64)
+    return math.sqrt(capi.frob_inner(d, d))
+
+
+def is_critical(x, s, tau_probe: float, eps: float, ctx: capi.Context | None = None) -> bool:
+    if not tau_probe > 0.0:
+        raise InvalidInput("is_critical: tau_probe must be positive")
+    return projection_residual(x, s, tau_probe, ctx) <= eps
+
+
+def is_interior(x: np.ndarray, eps_active: float) -> bool:
+    return bool(np.all(np.asarray(x) > eps_active))
+
+
+class _SplitMix64:                   # rng.hpp:14-34
+    def __init__(self, seed):
+        self.state = seed & 0xFFFFFFFFFFFFFFFF
+
+    def next(self):
+        self.state = (self.state + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+        z = self.state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+        return z ^ (z >> 31)
+
+    def next_double(self):
+        return float(self.next() >> 11) * 2.0 ** -53
+
+    def next_below(self, bound):
+        return self.next() % bound
+
+
+def _sparse_frob_inner(a: dict, b_dense=None, b: dict | None = None) -> float:
+    """frob_inner restricted to nonzeros, in storage order (node, then row): exact."""
+    acc = 0.0
+    for key in sorted(a):
+        other = b.get(key, 0.0) if b is not None else float(b_dense[key])
+        acc += a[key] * other
+    return acc
+
+
+def _random_directions(x, grad, triples, cfg: SecondOrderConfig) -> list:
+    """secondorder.hpp:158-189: random nonnegative combinations of kept pairs, rescaled to
+    ||V|| = sqrt(2), deduplicated (as sparse {(node, row): value} maps)."""
+    out = []
+    if triples is None or cfg.random_directions <= 0 or len(triples) == 0:
+        return out
+    npairs = len(triples)
+    pair_set = {(int(i), int(k), int(l)) for i, k, l in triples.tolist()}
+    rng = _SplitMix64(cfg.seed)
+    target = math.sqrt(2.0)
+    produced = attempts = 0
+    while produced < cfg.random_directions and attempts < 20 * cfg.random_directions:
+        attempts += 1
+        v: dict = {}
+        picks = 2 + rng.next_below(min(npairs, 6))
+        for _ in range(picks):
+            i, k, l = (int(t) for t in triples[rng.next_below(npairs)])
+            coeff = rng.next_double()
+            v[(i, k)] = v.get((i, k), 0.0) + coeff
+            v[(i, l)] = v.get((i, l), 0.0) - coeff
+        norm = math.sqrt(_sparse_frob_inner(v, b=v))
+        if norm == 0.0:
+            continue
+        scale = target / norm
+        v = {key: val * scale for key, val in v.items()}
+        if abs(_sparse_frob_inner(v, b_dense=grad)) / target > cfg.eps_grad_orth:
+            continue
+        if not _tangent_cone_contains_sparse(x, v, cfg.eps_cone, cfg.eps_active):
+            continue
+        nz = {key: val for key, val in v.items() if val != 0.0}
+        dup = False
+        if len(nz) == 2:                  # equal to a pair direction?
+            (a1, v1), (a2, v2) = sorted(nz.items())
+            if a1[0] == a2[0] and {v1, v2} == {1.0, -1.0}:
+                plus, minus = (a1[1], a2[1]) if v1 == 1.0 else (a2[1], a1[1])
+                dup = (a1[0], plus, minus) in pair_set
+        if not dup:
+            dup = any(nz == e for e in out)
+        if dup:
+            continue
+        out.append(nz)
+        produced += 1
+    return out
+
+
+def _tangent_cone_contains_sparse(x, v: dict, eps: float, eps_active: float) -> bool:
+    cols: dict = {}
+    for (i, k) in sorted(v):
+        cols.setdefault(i, []).append(k)
+    for i, ks in cols.items():
+        ssum = 0.0
+        for k in range(x.shape[1]):
+            val = v.get((i, k), 0.0)
+            ssum += val
+            if x[i, k] <= eps_active and val < -eps:
+                return False
+        if abs(ssum) > eps:
+            return False
+    return True
+
+
+def _dense(v: dict, shape) -> np.ndarray:
+    d = np.zeros(shape)
+    for (i, k), val in v.items():
+        d[i, k] = val
+    return d
+
+
+def refine(x: np.ndarray, s: SparseSimilarity, cfg: SecondOrderConfig | None = None,
+           ctx: capi.Context | None = None) -> RefinementReport:
+    """secondorder.hpp:343-368.  Pair directions are evaluated on the device in one batched
+    pass (fc_refine_pairs: bit-identical closed forms of the reference's HVP path, no
+    direction materialised); random combinations go through the device HVP."""
+    cfg = cfg or SecondOrderConfig()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    validate_membership(x, 1e-6)
+    c = _ctx_for(s, ctx)
+    rep = RefinementReport()
+    rep.residual = projection_residual(x, s, cfg.tau_probe, c)
+    rep.critical = rep.residual <= cfg.eps_critical
+    if not rep.critical:
+        rep.status = RefinementStatus.kRefutedFirstOrder
+        return rep
+    grad = full_gradient(x, s, c)
+    pr = c.refine_pairs(x, grad, cfg.eps_active, cfg.eps_grad_orth, cfg.budget,
+                        want_triples=cfg.random_directions > 0)
+    rnd = _random_directions(x, grad, pr["triples"], cfg)
+    npairs = int(pr["pairs"])
+    rep.directions_generated = npairs + len(rnd)
+    total = rep.directions_generated
+    budget = cfg.budget
+    # ---- condition (a): pairs first (device), then the random combinations in order
+    a = RefinementVerdict(directions_tested=min(total, budget))
+    worst, wit = pr["a_worst"], None
+    if pr["a_index"] != 2**64 - 1:
+        wit = {(pr["a_col"], pr["a_plus"]): 1.0, (pr["a_col"], pr["a_minus"]): -1.0}
+    for t, v in enumerate(rnd):
+        if npairs + t >= budget:
+            break
+        vd = _dense(v, x.shape)
+        q = capi.frob_inner(c.hessian_vector_product(x, vd), vd)
+        if q < worst:
+            worst, wit = q, v
+    if worst < -cfg.eps_quad:
+        a.status, a.witness, a.witness_value = RefinementStatus.kRefutedConditionA, wit, worst
+    rep.condition_a = a
+    if a.status == RefinementStatus.kRefutedConditionA:
+        rep.status = a.status
+        return rep
+    # ---- condition (b)
+    b = RefinementVerdict()
+    if is_interior(x, cfg.eps_active):
+        b.used_interior_shortcut = True
+    else:
+        b.directions_tested = min(total, budget)
+        worst, wit, base = pr["b_worst"], None, None
+        if pr["b_index"] != 2**64 - 1:
+            wit = {(pr["b_col"], pr["b_plus"]): 1.0, (pr["b_col"], pr["b_minus"]): -1.0}
+            base = {(pr["b_col"], pr["b_base_plus"]): 1.0, (pr["b_col"], pr["b_base_minus"]): -1.0}
+        for t, v in enumerate(rnd):
+            if npairs + t >= budget:
+                break
+            for i in sorted({key[0] for key in v}):
+                xi, gi = x[i], grad[i]
+                for l in range(x.shape[1]):
+                    if not (xi[l] <= cfg.eps_active and abs(v.get((i, l), 0.0)) > cfg.eps_active):
+                        continue
+                    for k in range(x.shape[1]):
+                        if k == l:
+                            continue
+                        val = float(gi[k] - gi[l])
+                        if val < worst:
+                            worst = val
+                            wit = {(i, k): 1.0, (i, l): -1.0}
+                            base = v
+        if worst < -cfg.eps_quad:
+            b.status, b.witness, b.witness_base, b.witness_value = (RefinementStatus.kRefutedConditionB, wit, base,
+                                                                    worst)
+    rep.condition_b = b
+    rep.status = b.status
+    return rep
+
+
 # ---- binary artifacts (new, SURVEY.md 8(d) / 8(f)4; same layouts as the C++ headers) -------
 _MEMB_MAGIC = b"FCMEMB01"
 _CSR_MAGIC = b"FCCSR001"

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.environ.get("FC_LIB") or os.path.join(LIBDIR, "libfuzzyclust_cuda.so")
-SOURCES = [os.path.join(CSRC, "fc_capi.cu"), os.path.join(CSRC, "fc_build.cu"), os.path.join(CSRC, "fc_ingest.cu"), os.path.join(CSRC, "generator.cpp")]
+SOURCES = [os.path.join(CSRC, "fc_capi.cu"), os.path.join(CSRC, "fc_build.cu"), os.path.join(CSRC, "fc_ingest.cu"), os.path.join(CSRC, "fc_refine.cu"), os.path.join(CSRC, "generator.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "fc_kernels.cuh"), os.path.join(CSRC, "fc_internal.h"),
                   os.path.join(ROOT, "include", "fuzzyclust_cuda.h")]
 

@@ -47,6 +47,13 @@ class GraphSpecC(C.Structure):
 
 
 # every symbol include/fuzzyclust_cuda.h declares: (restype, argtypes)
+class RefinePairsC(C.Structure):
+    _fields_ = [("pairs", C.c_uint64), ("a_worst", C.c_double), ("a_index", C.c_uint64), ("a_col", C.c_uint32),
+                ("a_plus", C.c_uint32), ("a_minus", C.c_uint32), ("pad0", C.c_uint32), ("b_worst", C.c_double),
+                ("b_index", C.c_uint64), ("b_col", C.c_uint32), ("b_plus", C.c_uint32), ("b_minus", C.c_uint32),
+                ("b_base_plus", C.c_uint32), ("b_base_minus", C.c_uint32), ("pad1", C.c_uint32)]
+
+
 SIGNATURES = {
     "fc_version": (C.c_char_p, []),
     "fc_abi_version": (C.c_int, []),
@@ -86,6 +93,8 @@ SIGNATURES = {
     "fc_cross_share": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp]),
     "fc_hessian_vector_product": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, _dp]),
     "fc_frob_inner": (C.c_double, [_dp, _dp, C.c_uint64]),
+    "fc_refine_pairs": (C.c_int, [C.c_void_p, C.c_uint32, _dp, _dp, C.c_double, C.c_double, C.c_uint64, _u32p,
+                                  C.c_uint64, C.POINTER(RefinePairsC)]),
     "fc_ingest_edge_list": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int, C.c_void_p]),
     "fc_graph_lcc_nodes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _u32p, C.POINTER(_u32p),
                                      C.POINTER(C.c_uint64)]),
@@ -242,6 +251,25 @@ class Context:
 
     def two_core_nodes(self, num_nodes, edges):
         return self._graph_nodes(lib().fc_graph_two_core_nodes, num_nodes, edges)
+
+    def refine_pairs(self, x, grad, eps_active, eps_grad_orth, budget, want_triples=False):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        grad = np.ascontiguousarray(grad, dtype=np.float64)
+        r = RefinePairsC()
+        cap = 0
+        tri = None
+        if want_triples:
+            # count first (a cheap pass), then fetch the list
+            self._c(lib().fc_refine_pairs(self.h, x.shape[1], _p(x), _p(grad), eps_active, eps_grad_orth, 0, None,
+                                          0, C.byref(r)))
+            cap = int(r.pairs)
+            tri = np.empty((max(cap, 1), 3), np.uint32)
+        self._c(lib().fc_refine_pairs(self.h, x.shape[1], _p(x), _p(grad), eps_active, eps_grad_orth,
+                                      min(int(budget), 2**64 - 1), _p(tri, _u32p) if want_triples else None, cap,
+                                      C.byref(r)))
+        out = {f: getattr(r, f) for f, _ in RefinePairsC._fields_ if not f.startswith("pad")}
+        out["triples"] = tri[:cap] if want_triples else None
+        return out
 
     def cross_share(self, a, b):
         a = np.ascontiguousarray(a, dtype=np.float64)

@@ -988,6 +988,15 @@ static int upload_csr_impl(fc_ctx*, uint64_t, uint64_t, const int64_t*, const ui
                            int);
 }
 int fc_internal_h2d(fc_ctx* ctx, void* dst, const void* src, size_t bytes) { return h2d_big(ctx, dst, src, bytes); }
+int fc_internal_csr(fc_ctx* ctx, uint64_t* n, const long long** row_ptr, const unsigned** col, const double** val) {
+    if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
+    if (ctx->comm) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
+    *n = ctx->n;
+    *row_ptr = ctx->d_row_ptr;
+    *col = ctx->d_col;
+    *val = ctx->weighted ? ctx->d_val : nullptr;
+    return FC_OK;
+}
 int fc_internal_d2h(fc_ctx* ctx, void* dst, const void* src, size_t bytes) { return d2h_big(ctx, dst, src, bytes); }
 int fc_internal_adopt_device_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t* h_row_ptr,
                                  const uint32_t* d_col, const double* d_val, double frob_sq) {

@@ -18,3 +18,6 @@ int fc_internal_adopt_device_csr(fc_ctx* ctx, uint64_t n, uint64_t nnz, const in
 // consumed, stream-ordered; d2h: synchronous)
 int fc_internal_h2d(fc_ctx* ctx, void* dst, const void* src, size_t bytes);
 int fc_internal_d2h(fc_ctx* ctx, void* dst, const void* src, size_t bytes);
+// the resident CSR of a single-rank context (all rows): n, row_ptr, col (hot bit
+// possible in bit 31), values (NULL = pattern)
+int fc_internal_csr(fc_ctx* ctx, uint64_t* n, const long long** row_ptr, const unsigned** col, const double** val);
