@@ -2032,14 +2032,31 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
     for (unsigned long long rb = (unsigned long long)blockIdx.x * R; rb < g.nrows;
          rb += (unsigned long long)gridDim.x * R) {
         const int rows = (int)min((unsigned long long)R, g.nrows - rb);
-        // 1: stage rows
-        for (int e = tid; e < rows * C; e += kWideThreads) {
-            const int r = e / C, k = e % C;
-            const size_t a = (size_t)(g.row0 + rb + r) * C + k;
-            const double av = A[a];
-            TX[r * LD + k] = (mode == kLiteral) ? av : extrap(av, Bp[a], beta);
-            TY[r * LD + k] = XS[(size_t)(rb + r) * C + k];
+        // 1: stage rows through cp.async: A -> TX, B -> TY, X_ext formed in place in TX,
+        //    then S X_ext -> TY, which lands while the GEMM runs
+        for (int e = tid; e < rows * CP; e += kWideThreads) {
+            const int r = e / CP, k = e % CP;                // CP constexpr: shifts
+            if (k < C) {
+                const size_t a = (size_t)(g.row0 + rb + r) * C + k;
+                cp_async8(TX + r * LD + k, A + a);
+                if (mode != kLiteral) cp_async8(TY + r * LD + k, Bp + a);
+            }
         }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        if (mode != kLiteral) {
+            for (int e = tid; e < rows * CP; e += kWideThreads) {
+                const int r = e / CP, k = e % CP;
+                if (k < C) TX[r * LD + k] = extrap(TX[r * LD + k], TY[r * LD + k], beta);
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < rows * CP; e += kWideThreads) {
+            const int r = e / CP, k = e % CP;
+            if (k < C) cp_async8(TY + r * LD + k, XS + (size_t)(rb + r) * C + k);
+        }
+        cp_async_commit();
         // 2: GEMM over l-chunks of G
         auto stage_g = [&](int buf, int l0) {
             const int nl = min(kWideLC, C - l0);
@@ -2058,6 +2075,8 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
         stage_g(0, 0);
         int buf = 0;
         for (int l0 = 0; l0 < C; l0 += kWideLC, buf ^= 1) {
+            // groups in flight: S X_ext rows, G chunk l0 [, G chunk l0 + LC]; the rows'
+            // group is the oldest, so waiting for chunk l0 covers it too
             if (l0 + kWideLC < C) {
                 stage_g(buf ^ 1, l0 + kWideLC);
                 cp_async_wait_1();
@@ -2178,9 +2197,9 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
         if (live && row_fin && C == 1 && pq == 0) ty[0] = 1.0;
         __syncthreads();
         // 5: store bar^n
-        for (int e = tid; e < rows * C; e += kWideThreads) {
-            const int r = e / C, k = e % C;
-            D[(size_t)(g.row0 + rb + r) * C + k] = TY[r * LD + k];
+        for (int e = tid; e < rows * CP; e += kWideThreads) {
+            const int r = e / CP, k = e % CP;
+            if (k < C) D[(size_t)(g.row0 + rb + r) * C + k] = TY[r * LD + k];
         }
         __syncthreads();
     }
