@@ -630,16 +630,20 @@ int phase_gram(fc_ctx* ctx, bool dual) {
     const uint32_t c = ctx->c;
     // few 1024-row blocks (small N): one thread per (r, s) pair, larger chunks (fewer barriers)
     const bool few = ctx->local_blocks < (uint64_t)ctx->sm_count * 2;
-    const int TS = few ? 1 : 4;
+    // 8x8 tiles from C = 64 (fewer shared loads per FP64 pair, and one CTA covers all
+    // tiles of a block instead of re-staging its rows for several tile groups)
+    const int TS = few ? 1 : (c >= 64 ? 8 : 4);
     const int nT = ((int)c + TS - 1) / TS;
     const int tiles = nT * (nT + 1) / 2 * (dual ? 2 : 1);
     int R = gram_rows_per_chunk(c);
     if (few) R = std::max(R, std::min(128, 4096 / (int)((c + 3) & ~3u)));
-    const size_t smem = gram_smem((int)c, dual ? 1 : 0, R);
-    static size_t smem_set[2] = {0, 0};
-    if (smem > 48 * 1024 && smem > smem_set[few]) {
-        CU(cudaFuncSetAttribute(few ? k_gram<1> : k_gram<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set[few] = smem;
+    if (TS == 8) R = std::max(8, std::min(16, 2048 / (int)((c + 7) & ~7u)));
+    const size_t smem = gram_smem((int)c, dual ? 1 : 0, R, TS);
+    static size_t smem_set[9] = {0};
+    auto kfn = TS == 1 ? k_gram<1> : (TS == 8 ? k_gram<8> : k_gram<4>);
+    if (smem > 48 * 1024 && smem > smem_set[TS]) {
+        CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set[TS] = smem;
     }
     for (size_t s = 0; s < ctx->shards.size(); ++s) {
         const Geo g = make_geo(ctx, s);
@@ -647,8 +651,7 @@ int phase_gram(fc_ctx* ctx, bool dual) {
         const Bufs b = make_bufs(ctx, s);
         const int threads = std::min(kGramMaxThreads, (tiles + 31) / 32 * 32);
         dim3 grid((unsigned)g.nblk, (unsigned)((tiles + threads - 1) / threads));
-        if (few) k_gram<1><<<grid, threads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
-        else k_gram<4><<<grid, threads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
+        kfn<<<grid, threads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
         TRY(check_launch(ctx, "k_gram"));
     }
     return FC_OK;

@@ -957,11 +957,12 @@ __global__ void __launch_bounds__(kRowsumThreads) k_rowsum(Bufs b, Geo g, int ns
 // (formed as in solver.hpp:261); single: matrix 0 = the swept point.
 // grid = (blocks, tile groups); blockDim = 128.
 // =============================================================================
-constexpr int kGramMaxThreads = 256;   // blockDim = min(256, tiles rounded up to a warp)
+constexpr int kGramMaxThreads = 320;   // blockDim = min(320, tiles rounded up to a warp)
 
 // Shared memory of k_gram: 2 stages x (bar [+ prev]) x R x C4, + the ext tile (dual).
-__host__ __device__ inline size_t gram_smem(int C, int dual, int R) {
-    const int C4 = (C + 3) & ~3;
+__host__ __device__ inline size_t gram_smem(int C, int dual, int R, int TS = 4) {
+    const int PADW = TS > 4 ? TS : 4;
+    const int C4 = (C + PADW - 1) / PADW * PADW;
     return sizeof(double) * (size_t)R * C4 * (dual ? 5 : 2);
 }
 
@@ -974,7 +975,8 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
     if (st->done) return;
     extern __shared__ double smg[];
     const int C = (int)g.C;
-    const int C4 = (C + 3) & ~3;
+    constexpr int PADW = TS > 4 ? TS : 4;
+    const int C4 = (C + PADW - 1) / PADW * PADW;         // row stride in shared memory
     const int nT = (C + TS - 1) / TS;
     const int tiles_per_mat = nT * (nT + 1) / 2;
     const int nmat = dual ? 2 : 1;
@@ -1042,7 +1044,17 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
             const double* t = mat_local == 0 ? tb : te;
             for (int rr = 0; rr < rows; ++rr) {
                 double xr[TS], xq[TS];
-                if constexpr (TS == 4) {
+                if constexpr (TS == 8) {
+                    const double2* rowp = reinterpret_cast<const double2*>(t + rr * C4);
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        const double2 rv = rowp[4 * I + a], qv = rowp[4 * J + a];
+                        xr[2 * a] = rv.x;
+                        xr[2 * a + 1] = rv.y;
+                        xq[2 * a] = qv.x;
+                        xq[2 * a + 1] = qv.y;
+                    }
+                } else if constexpr (TS == 4) {
                     const double2* rowp = reinterpret_cast<const double2*>(t + rr * C4);
                     const double2 r01 = rowp[2 * I], r23 = rowp[2 * I + 1];
                     const double2 q01 = rowp[2 * J], q23 = rowp[2 * J + 1];

@@ -334,3 +334,20 @@ def test_heavy_row_phase_bitwise(oracle, c, vshards, monkeypatch):
             assert np.array_equal(xs, xs_o) and m == m_o
     finally:
         t.close()
+
+
+# ---- Gram tile shapes of the many-block path (TS = 4, TS = 8 from C = 64) -------------------
+@pytest.mark.parametrize("c", [32, 64, 72])
+def test_many_block_gram_tiles_bitwise(oracle, c):
+    """N = 310k (303 blocks of 1024 rows, more than 2 per SM): k_gram's 4x4 (C < 64) and
+    8x8 (C >= 64, C = 72 exercises the padded width) register tiles vs the oracle."""
+    g = random_graph(310_000, 5.0, 40 + c)
+    x0 = oracle.init_random(g.n, c, 3)
+    t = capi.Context(0)
+    try:
+        t.upload(g)
+        kw = dict(method=FISTA, max_iter=2, fista_restart=True)
+        assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+        assert t.share_matrix(x0).tobytes() == oracle.share_matrix(x0).tobytes()
+    finally:
+        t.close()
