@@ -632,7 +632,11 @@ int phase_gram(fc_ctx* ctx, bool dual) {
     const bool few = ctx->local_blocks < (uint64_t)ctx->sm_count * 2;
     // 8x8 tiles from C = 64 (fewer shared loads per FP64 pair, and one CTA covers all
     // tiles of a block instead of re-staging its rows for several tile groups)
-    const int TS = few ? 1 : (c >= 64 ? 8 : 4);
+    int TS = few ? 1 : (c >= 64 ? 8 : 4);
+    if (const char* e = std::getenv("FC_GRAM_TS")) {
+        const int v = std::atoi(e);
+        if (v == 1 || v == 4 || v == 8) TS = v;
+    }
     const int nT = ((int)c + TS - 1) / TS;
     const int tiles = nT * (nT + 1) / 2 * (dual ? 2 : 1);
     int R = gram_rows_per_chunk(c);
