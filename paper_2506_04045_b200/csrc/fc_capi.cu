@@ -1253,8 +1253,21 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
         for (size_t sh = 0; sh < ctx->shards.size(); ++sh) {
             const Shard& S = ctx->shards[sh];
             const size_t first = heavy.size();
-            for (uint64_t i = S.row0; i < S.row0 + S.nrows; ++i)
-                if (deg(i) >= ctx->heavy_deg) heavy.push_back((unsigned)(i - S.row0));
+            // scan the shard's row_ptr with the copy threads (row order kept chunk by chunk)
+            const int nt = S.nrows >= (uint64_t(1) << 20) ? std::max(1, ctx->copy_threads) : 1;
+            std::vector<std::vector<unsigned>> part(nt);
+            auto scan = [&](int t) {
+                const uint64_t a = S.row0 + S.nrows * t / nt, e = S.row0 + S.nrows * (t + 1) / nt;
+                for (uint64_t i = a; i < e; ++i)
+                    if (deg(i) >= ctx->heavy_deg) part[t].push_back((unsigned)(i - S.row0));
+            };
+            {
+                std::vector<std::thread> th;
+                for (int t = 1; t < nt; ++t) th.emplace_back(scan, t);
+                scan(0);
+                for (auto& x : th) x.join();
+            }
+            for (auto& pv : part) heavy.insert(heavy.end(), pv.begin(), pv.end());
             std::stable_sort(heavy.begin() + first, heavy.end(),
                              [&](unsigned a, unsigned b2) { return deg(S.row0 + a) > deg(S.row0 + b2); });
             ctx->heavy_off[sh] = first;
