@@ -287,6 +287,14 @@ int by_c(fc_ctx* ctx, uint32_t c, A&&... a) {
     return set_err(ctx, FC_INVALID, "cluster count C=%u exceeds the supported maximum 256", c);
 }
 
+// Launch-configuration caches are per device: cudaFuncSetAttribute applies to the
+// current device, and a process may drive several contexts on several GPUs.
+template <class T>
+struct PerDevice {
+    T v[64] = {};
+    T& operator()(const fc_ctx* ctx) { return v[ctx->device & 63]; }
+};
+
 int grid_for(const void* fn, int threads, size_t smem, int sm_count) {
     int occ = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1) occ = 1;
@@ -295,7 +303,8 @@ int grid_for(const void* fn, int threads, size_t smem, int sm_count) {
 
 template <int G, int S, bool DUAL, bool W, bool EXACT>
 int launch_sweep_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
-    static int grid = 0;
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
     if (!grid) grid = grid_for((const void*)k_sweep<G, S, DUAL, W, EXACT>, 256, 0, ctx->sm_count);
     const unsigned long long need = (g.nrows + g.chunk - 1) / g.chunk;   // row chunks, 8 warps per CTA
     const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, (need + 7) / 8));
@@ -308,9 +317,11 @@ int launch_sweep_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
 
 template <int S, bool DUAL>
 int launch_sweep_tma(fc_ctx* ctx, const Bufs& b, const Geo& g) {
-    static int grid = 0;
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
     const size_t smem = sweep_tma_smem((int)g.C, DUAL ? 1 : 0);
-    static size_t smem_set = 0;
+    static PerDevice<size_t> smem_set_pd;
+    size_t& smem_set = smem_set_pd(ctx);
     if (smem > smem_set) {
         CU(cudaFuncSetAttribute(k_sweep_tma<S, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         smem_set = smem;
@@ -327,7 +338,8 @@ int launch_sweep_tma(fc_ctx* ctx, const Bufs& b, const Geo& g) {
 
 template <int G, bool DUAL, bool W>
 int launch_sweep_small(fc_ctx* ctx, const Bufs& b, const Geo& g) {
-    static int grid = 0;
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
     if (!grid) grid = grid_for((const void*)k_sweep_small<G, DUAL, W>, 256, 0, ctx->sm_count);
     const unsigned long long need = (g.nrows + g.chunk - 1) / g.chunk;
     const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, (need + 7) / 8));
@@ -369,7 +381,8 @@ struct LaunchSweep {
 
 template <int G, bool EXACT>
 int launch_step_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
-    static int grid = 0;
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
     const size_t smem = step_t_smem(G);
     if (!grid) {
         CU(cudaFuncSetAttribute(k_step_t<G, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -386,7 +399,8 @@ int launch_step_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
 
 template <int CP>
 int launch_step_big(fc_ctx* ctx, const Bufs& b, const Geo& g) {
-    static int grid = 0;
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
     const size_t smem = StepBigCfg<CP>::smem();
     if (!grid) {
         CU(cudaFuncSetAttribute(k_step_big<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -404,7 +418,8 @@ int launch_step_big(fc_ctx* ctx, const Bufs& b, const Geo& g) {
 
 template <int CP>
 int launch_step_wide(fc_ctx* ctx, const Bufs& b, const Geo& g) {
-    static int grid = 0;
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
     const size_t smem = WideCfg<CP>::smem();
     if (!grid) {
         CU(cudaFuncSetAttribute(k_step_wide<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -429,7 +444,8 @@ struct LaunchStep {
         if (S == 1 && !bt) {   // thread-per-row projection
             return g.C == (unsigned)G ? launch_step_t<G, true>(ctx, b, g) : launch_step_t<G, false>(ctx, b, g);
         }
-        static int grid = 0;
+        static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
         if (!grid) grid = grid_for((const void*)k_step<G, S>, 256, 0, ctx->sm_count);
         const unsigned long long need = (g.nrows + (32 / G) * 8 - 1) / ((32 / G) * 8);
         const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
@@ -643,7 +659,8 @@ int phase_gram(fc_ctx* ctx, bool dual) {
     if (few) R = std::max(R, std::min(128, 4096 / (int)((c + 3) & ~3u)));
     if (TS == 8) R = std::max(8, std::min(16, 2048 / (int)((c + 7) & ~7u)));
     const size_t smem = gram_smem((int)c, dual ? 1 : 0, R, TS);
-    static size_t smem_set[9] = {0};
+    static PerDevice<size_t[9]> smem_set_pd;
+    size_t (&smem_set)[9] = smem_set_pd(ctx);
     auto kfn = TS == 1 ? k_gram<1> : (TS == 8 ? k_gram<8> : k_gram<4>);
     if (smem > 48 * 1024 && smem > smem_set[TS]) {
         CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
