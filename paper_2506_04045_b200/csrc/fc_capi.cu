@@ -379,18 +379,18 @@ struct LaunchSweep {
     }
 };
 
-template <int G, bool EXACT>
+template <int G, bool EXACT, bool BT>
 int launch_step_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     static PerDevice<int> grid_pd;
     int& grid = grid_pd(ctx);
     const size_t smem = step_t_smem(G);
     if (!grid) {
-        CU(cudaFuncSetAttribute(k_step_t<G, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        grid = grid_for((const void*)k_step_t<G, EXACT>, kStepThreads, smem, ctx->sm_count);
+        CU(cudaFuncSetAttribute(k_step_t<G, EXACT, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_t<G, EXACT, BT>, kStepThreads, smem, ctx->sm_count);
     }
     const unsigned long long need = (g.nrows + 32 * (kStepThreads / 32) - 1) / (32 * (kStepThreads / 32));
     const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
-    k_step_t<G, EXACT><<<gr, kStepThreads, smem, ctx->stream>>>(b, g);
+    k_step_t<G, EXACT, BT><<<gr, kStepThreads, smem, ctx->stream>>>(b, g);
     ctx->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_t launch: %s", cudaGetErrorString(e));
@@ -441,8 +441,12 @@ struct LaunchStep {
         if constexpr (S > 1) {
             if (!bt) return ctx->step_big ? launch_step_big<32 * S>(ctx, b, g) : launch_step_wide<32 * S>(ctx, b, g);
         }
-        if (S == 1 && !bt) {   // thread-per-row projection
-            return g.C == (unsigned)G ? launch_step_t<G, true>(ctx, b, g) : launch_step_t<G, false>(ctx, b, g);
+        if (S == 1 && (!bt || G <= 16)) {   // thread-per-row projection (+ backtracking row terms;
+            // at G = 32 those spill, the lane-parallel k_step below takes bt there)
+            if (bt) return g.C == (unsigned)G ? launch_step_t<G, true, true>(ctx, b, g)
+                                              : launch_step_t<G, false, true>(ctx, b, g);
+            return g.C == (unsigned)G ? launch_step_t<G, true, false>(ctx, b, g)
+                                      : launch_step_t<G, false, false>(ctx, b, g);
         }
         static PerDevice<int> grid_pd;
     int& grid = grid_pd(ctx);

@@ -1691,7 +1691,9 @@ __device__ __forceinline__ void fold_residual(double (&w)[CP], int C) {
 // G (power of two, 2..32) is the padded row width, C <= G; EXACT: C == G.
 constexpr int kStepThreads = 128;
 
-template <int G, bool EXACT>
+// BT: also the backtracking row terms (as k_step): lin_i = sum_r g_r (bar_r - x_r),
+// sq_i = sum_r (bar_r - x_r)^2, <xs_i, x_i>; g is parked in the thread's A-tile row.
+template <int G, bool EXACT, bool BT = false>
 __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
     DevState* st = b.st;
     if (st->done) return;
@@ -1726,7 +1728,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
     const unsigned long long warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
     const bool lane_ok = EXACT || lg < C;
-    const double* ra = TA + lane * LD;                       // this thread's row in phase 2
+    double* ra = TA + lane * LD;                             // this thread's row in phase 2
     const double* rb_ = TB + lane * LD;
     double* tr = TX + lane * LD;
     bool bad = false;
@@ -1751,6 +1753,12 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
 #pragma unroll
             for (int l = 0; l < G; ++l)
                 xr[l] = (EXACT || l < C) ? ((mode == kLiteral) ? ra[l] : extrap(ra[l], rb_[l], beta)) : 0.0;
+            double mi = 0.0;                                 // BT: <xs_i, x_i>, component order
+            if constexpr (BT) {
+#pragma unroll
+                for (int k = 0; k < G; ++k)
+                    if (EXACT || k < C) mi = dadd(mi, dmul(tr[k], xr[k]));
+            }
             // gradient (objective.hpp:37-43, :116-117), KU independent chains
 #pragma unroll 1
             for (int k0 = 0; k0 < C; k0 += KU) {
@@ -1775,6 +1783,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
 #pragma unroll
             for (int k = 0; k < G; ++k) {
                 if (EXACT || k < C) {
+                    if constexpr (BT) ra[k] = tr[k];            // keep g_k for lin_i
                     const double y = dsub(xr[k], dmul(tau, tr[k]));
                     fin = fin && isfinite(y);
                     tr[k] = y;
@@ -1793,6 +1802,20 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
 #pragma unroll
                 for (int k = 0; k < G; ++k)
                     if (EXACT || k < C) tr[k] = w[k];
+            }
+            if constexpr (BT) {
+                double li = 0.0, qi = 0.0;
+#pragma unroll
+                for (int k = 0; k < G; ++k) {
+                    if (EXACT || k < C) {
+                        const double d = dsub(tr[k], xr[k]);
+                        li = dadd(li, dmul(ra[k], d));
+                        qi = dadd(qi, dmul(d, d));
+                    }
+                }
+                b.rowterm[0][rb + lane] = li;
+                b.rowterm[1][rb + lane] = qi;
+                b.rowterm[2][rb + lane] = mi;
             }
         }
         __syncwarp();
