@@ -235,10 +235,13 @@ def test_virtual_shards_bitwise(oracle, shards):
 
 
 # ---- backtracking (parity by restatement; unpinned by the reference) ---------------------------
-def test_backtracking_vs_restatement(ctx, oracle):
+@pytest.mark.parametrize("c", [3, 8, 12, 16, 32, 40])
+def test_backtracking_vs_restatement(ctx, oracle, c):
+    """k_step_t's backtracking row terms (C <= 16, exact and padded widths) and the
+    lane-parallel k_step (C = 32, 40) against the restatement."""
     g = random_graph(5000, 8.0, 13)
     ctx.upload(g)
-    x0 = oracle.init_random(g.n, 8, 7)
+    x0 = oracle.init_random(g.n, c, 7)
     tau = oracle.default_step_size(g)
     for kw in [dict(method=FISTA_BT, max_iter=25, fista_restart=True),
                dict(method=FISTA_BT, step_size=5000 * tau, max_iter=40, fista_restart=True, bt_eta=2.0, bt_max=60),
