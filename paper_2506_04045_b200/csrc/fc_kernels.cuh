@@ -359,10 +359,13 @@ __device__ __forceinline__ double group_seq_sum_m(const double (&a)[S], int C, u
 // =============================================================================
 // Gathers in flight per lane per batch (x2 when DUAL): measured at config C
 // (C=32) 16 -> 36.7 ms vs 8 -> 38.8 ms per sweep; C=16 (config B) prefers 8.
+#ifndef FC_SWEEP16_MINB
+#define FC_SWEEP16_MINB 4
+#endif
 template <int G, int S = 1>
 struct SweepTune {
     static constexpr int U = G == 32 ? (16 / S > 2 ? 16 / S : 2) : (G < 8 ? G : 8);
-    static constexpr int MINB = G == 32 ? (S == 1 ? 3 : 2) : 4;     // CTAs per SM (register budget)
+    static constexpr int MINB = G == 32 ? (S == 1 ? 3 : 2) : (G == 16 ? FC_SWEEP16_MINB : 4);   // CTAs per SM
 };
 
 template <int G, int S, bool DUAL, bool W, bool EXACT>
