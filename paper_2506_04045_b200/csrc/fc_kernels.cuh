@@ -160,6 +160,8 @@ constexpr unsigned kHotBit = 0x80000000u;
 constexpr unsigned kIdxMask = 0x7fffffffu;
 
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __host__ __device__ __forceinline__ unsigned pair_index(unsigned r, unsigned s, unsigned C) {
     // packed upper triangle, r <= s, row-major
@@ -1103,13 +1105,16 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
 // =============================================================================
 constexpr int kCombTile = 128;
 constexpr int kCombThreads = 256;
-constexpr size_t kCombSmem = 2 * kCombTile * 32 * sizeof(double);
+constexpr int kCombStages = 4;                                // tiles in flight per CTA
+constexpr size_t kCombSmem = (size_t)kCombStages * kCombTile * 32 * sizeof(double);
 
-
+// Every thread loads one chain column (lane) of 16 block rows per tile through a
+// kCombStages-deep cp.async ring (source pointers hoisted: one add per element);
+// warp 0 (lane = chain) adds the landed tiles in ascending block order.
 __global__ void __launch_bounds__(kCombThreads) k_combine(Bufs b, Geo g, int mat_mask, int scal_mask,
                                                           const double* init) {
     if (b.st->done) return;
-    extern __shared__ double ctile[];                       // [2][kCombTile][32]
+    extern __shared__ double ctile[];                       // [kCombStages][kCombTile][32]
     const int np = (int)g.npairs;
     const int mat_groups = (2 * np + 31) / 32;
     const double* sbase = nullptr;
@@ -1130,33 +1135,43 @@ __global__ void __launch_bounds__(kCombThreads) k_combine(Bufs b, Geo g, int mat
     if (!sbase && live) live = (mat_mask >> (my_c / np)) & 1;
     const unsigned long long nb = g.nblk;
     const unsigned long long ntiles = (nb + kCombTile - 1) / kCombTile;
-    // loaders: every thread of warps 1..7 (all warps for the first tile) copies
-    // (block, chain) elements of a tile straight into shared memory
-    auto stage = [&](int buf, unsigned long long t, int t0, int stride) {
-        double* dst = ctile + (size_t)buf * kCombTile * 32;
-        const unsigned long long b0 = t * kCombTile;
-        for (int e = t0; e < kCombTile * 32; e += stride) {
-            const int r = e >> 5, c = e & 31;
-            const unsigned long long blk = b0 + r;
-            const int cc = c0 + c;
-            const double* src = nullptr;
-            if (blk < nb && c < nch) {
-                if (sbase) src = sbase + blk;
-                else if ((mat_mask >> (cc / np)) & 1) src = b.gpart[cc / np] + blk * (size_t)np + (cc % np);
-            }
-            if (src) cp_async8(dst + e, src);
-            else dst[e] = 0.0;
+    // this thread's column source: block partial blk of chain my_c at col + blk * step
+    const double* col = nullptr;
+    size_t step = 0;
+    if (live) {
+        if (sbase) {
+            col = sbase;
+            step = 1;
+        } else {
+            col = b.gpart[my_c / np] + (my_c % np);
+            step = (size_t)np;
         }
-        cp_async_commit();
+    }
+    constexpr int kRowsPerThread = kCombTile / (kCombThreads / 32);
+    auto stage = [&](unsigned long long t) {
+        double* dst = ctile + (size_t)(t % kCombStages) * kCombTile * 32 + lane;
+        const unsigned long long b0 = t * kCombTile;
+#pragma unroll 4
+        for (int i = 0; i < kRowsPerThread; ++i) {
+            const int r = warp + (kCombThreads / 32) * i;
+            const unsigned long long blk = b0 + r;
+            if (col && blk < nb) cp_async8(dst + r * 32, col + blk * step);
+            else dst[r * 32] = 0.0;
+        }
     };
     double acc = (live && init) ? init[my_c] : 0.0;
-    if (ntiles) stage(0, 0, threadIdx.x, kCombThreads);
-    cp_async_wait_all();
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kCombStages - 1; ++k) {
+        if ((unsigned long long)k < ntiles) stage(k);
+        cp_async_commit();
+    }
     for (unsigned long long t = 0; t < ntiles; ++t) {
-        const int buf = (int)(t & 1);
+        cp_async_wait_n<kCombStages - 2>();                  // tile t landed (own copies)
+        __syncthreads();                                     // ... everyone's; tile t-1 fully summed
+        if (t + kCombStages - 1 < ntiles) stage(t + kCombStages - 1);
+        cp_async_commit();
         if (warp == 0) {
-            const double* tl = ctile + (size_t)buf * kCombTile * 32 + lane;
+            const double* tl = ctile + (size_t)(t % kCombStages) * kCombTile * 32 + lane;
             const int rows = (int)min((unsigned long long)kCombTile, nb - t * kCombTile);
             if (rows == kCombTile) {
 #pragma unroll 16
@@ -1164,12 +1179,9 @@ __global__ void __launch_bounds__(kCombThreads) k_combine(Bufs b, Geo g, int mat
             } else {
                 for (int r = 0; r < rows; ++r) acc = dadd(acc, tl[r * 32]);
             }
-        } else if (t + 1 < ntiles) {
-            stage(buf ^ 1, t + 1, threadIdx.x - 32, kCombThreads - 32);
-            cp_async_wait_all();
         }
-        __syncthreads();
     }
+    cp_async_wait_all();
     if (warp == 0 && live) b.totals[my_c] = acc;
 }
 
