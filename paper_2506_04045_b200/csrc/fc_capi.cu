@@ -94,6 +94,9 @@ struct CopyPool {
 struct fc_ctx {
     int device = 0, rank = 0, world = 1, vshards = 1;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;       // Gram next to the sweep (independent within an iteration)
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    bool overlap = false;              // FC_OVERLAP=1: Gram on a side stream (measured: no gain)
     ncclComm_t comm = nullptr;
     int sm_count = 148;
     std::string err;
@@ -645,7 +648,8 @@ int phase_step(fc_ctx* ctx, int bt) {
     return FC_OK;
 }
 
-int phase_gram(fc_ctx* ctx, bool dual) {
+int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr) {
+    if (!strm) strm = ctx->stream;
     ProfScope p(ctx, kClsGram);
     const uint32_t c = ctx->c;
     // few 1024-row blocks (small N): one thread per (r, s) pair, larger chunks (fewer barriers)
@@ -676,7 +680,7 @@ int phase_gram(fc_ctx* ctx, bool dual) {
         const Bufs b = make_bufs(ctx, s);
         const int threads = std::min(kGramMaxThreads, (tiles + 31) / 32 * 32);
         dim3 grid((unsigned)g.nblk, (unsigned)((tiles + threads - 1) / threads));
-        kfn<<<grid, threads, smem, ctx->stream>>>(b, g, dual ? 1 : 0, R);
+        kfn<<<grid, threads, smem, strm>>>(b, g, dual ? 1 : 0, R);
         TRY(check_launch(ctx, "k_gram"));
     }
     return FC_OK;
@@ -778,11 +782,28 @@ int enqueue_prelude(fc_ctx* ctx) {   // FISTA loss at x0 (solver.hpp:206-212)
     return FC_OK;
 }
 
+// Gram and sweep of one iteration both only read the new iterate.  Opt-in
+// (FC_OVERLAP=1): the Gram on a side stream next to the sweep, launched after it so
+// the heavy rows start at once.  Measured no gain (the persistent sweep holds the
+// register file until its tail), so the default is sequential.
+static int gram_and_sweep(fc_ctx* ctx) {
+    if (ctx->overlap && !ctx->comm && !ctx->profiling) {
+        CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
+        CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+        TRY(phase_sweep(ctx, true));
+        TRY(phase_gram(ctx, true, ctx->side));
+        CU(cudaEventRecord(ctx->join_ev, ctx->side));
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+        return FC_OK;
+    }
+    TRY(phase_gram(ctx, true));
+    return phase_sweep(ctx, true);
+}
+
 int enqueue_fista_iteration(fc_ctx* ctx, int bt) {
     TRY(phase_step(ctx, bt));
     TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
-    TRY(phase_gram(ctx, true));
-    TRY(phase_sweep(ctx, true));
+    TRY(gram_and_sweep(ctx));
     TRY(phase_rowsum(ctx, bt));
     TRY(phase_combine(ctx, 3, bt ? 0xF : 1));
     TRY(phase_finalize(ctx, kFinFista, 3));
@@ -1083,6 +1104,10 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         if (const char* e = std::getenv("FC_COPY_THREADS")) ctx->copy_threads = std::max(1, std::atoi(e));
     }
     CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+    if (const char* ov = std::getenv("FC_OVERLAP")) ctx->overlap = std::strcmp(ov, "1") == 0;
     CU(cudaMalloc(&ctx->d_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_done, 2 * sizeof(int)));
@@ -1156,6 +1181,10 @@ void fc_destroy(fc_ctx* ctx) {
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
     if (ctx->h_done) cudaFreeHost(ctx->h_done);
     for (auto e : ctx->chunk_ev) if (e) cudaEventDestroy(e);
+    if (ctx->side) cudaStreamSynchronize(ctx->side);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
