@@ -468,6 +468,16 @@ template <int G, int S>
 struct LaunchProject {
     static int run(fc_ctx* ctx, double* x, unsigned long long rows, int c, unsigned* flag) {
         if (rows == 0) return FC_OK;
+        if constexpr (S == 1) {                              // thread per row
+            const unsigned long long need = (rows + 127) / 128;
+            const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(ctx->sm_count * 8, need));
+            if (c == G) k_project_t<G, true><<<gr, 128, 0, ctx->stream>>>(x, rows, c, flag);
+            else k_project_t<G, false><<<gr, 128, 0, ctx->stream>>>(x, rows, c, flag);
+            ctx->launches++;
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_project_t launch: %s", cudaGetErrorString(e));
+            return FC_OK;
+        }
         const unsigned long long need = (rows + (32 / G) * 8 - 1) / ((32 / G) * 8);
         const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(ctx->sm_count * 8, need));
         k_project<G, S><<<gr, 256, 0, ctx->stream>>>(x, rows, c, flag);

@@ -2261,6 +2261,62 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
 
 inline size_t step_t_smem(int G) { return sizeof(double) * ((size_t)G * G + (kStepThreads / 32) * 3 * 32 * (G + 1)); }
 
+// Batched in-place projection, C <= 32, thread per row (init_membership's
+// per-column projection and project_simplex): the step kernel's projection
+// (register bitonic sort, exact threshold, mask folds) without the gradient.
+// A warp stages 32 rows through a [32][G+1] tile (coalesced both ways).
+template <int G, bool EXACT>
+__global__ void __launch_bounds__(128) k_project_t(double* x, unsigned long long rows, int C, unsigned* bad_flag) {
+    constexpr int LD = G + 1;
+    constexpr int RPW = 32 / G;
+    __shared__ double tiles[4][32 * LD];
+    const unsigned lane = threadIdx.x & 31u;
+    const int lg = (int)(lane % G);
+    const int sub = (int)(lane / G);
+    double* T = tiles[threadIdx.x >> 5];
+    double* tr = T + lane * LD;
+    const bool lane_ok = EXACT || lg < C;
+    const unsigned long long warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    bool bad = false;
+    for (unsigned long long rb = w0 * 32; rb < rows; rb += warps * 32) {
+        for (int p = 0; p < 32; p += RPW) {
+            const unsigned long long row = rb + p + sub;
+            if (row < rows && lane_ok) T[(p + sub) * LD + lg] = x[row * C + lg];
+        }
+        __syncwarp();
+        if (rb + lane < rows) {
+            double w[G];
+            bool fin = true;
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                w[k] = (EXACT || k < C) ? tr[k] : 0.0;
+                if ((EXACT || k < C) && !isfinite(w[k])) fin = false;
+            }
+            if (!fin) {
+                bad = true;
+            } else if (C == 1) {
+                tr[0] = 1.0;
+            } else {
+                const double thr = row_threshold<G>(tr, C);
+#pragma unroll
+                for (int k = 0; k < G; ++k) w[k] = (EXACT || k < C) ? ref_max(dsub(w[k], thr), 0.0) : 0.0;
+                fold_residual<G>(w, C);
+#pragma unroll
+                for (int k = 0; k < G; ++k)
+                    if (EXACT || k < C) tr[k] = w[k];
+            }
+        }
+        __syncwarp();
+        for (int p = 0; p < 32; p += RPW) {
+            const unsigned long long row = rb + p + sub;
+            if (row < rows && lane_ok) x[row * C + lg] = T[(p + sub) * LD + lg];
+        }
+        __syncwarp();
+    }
+    if (bad) atomicOr(bad_flag, 1u);
+}
+
 // Batched in-place projection (init_membership's per-column projection).
 template <int G, int S>
 __global__ void __launch_bounds__(256) k_project(double* x, unsigned long long rows, int C,
