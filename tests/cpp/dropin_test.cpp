@@ -267,6 +267,32 @@ TEST(Graph, ParseLccCoreLikeGraphTest) {
     EXPECT_TRUE(is_connected(path));
 }
 
+TEST(Refine, UniformSaddleAtThreeClustersOnDevice) {
+    // secondorder_test.cpp: the uniform point is a saddle; <H V, V> = -8 (C-1)/C
+    const auto s = seven();
+    const std::size_t c = 3;
+    MembershipMatrix x(c, 7);
+    for (double& e : x.data()) e = 1.0 / static_cast<double>(c);
+    SecondOrderConfig cfg;
+    const auto report = refine(x, s, cfg);
+    EXPECT_TRUE(report.critical);
+    EXPECT_TRUE(report.status == RefinementStatus::kRefutedConditionA);
+    EXPECT_NEAR(report.condition_a.witness_value, -8.0 * (c - 1) / c, 1e-9);
+    EXPECT_EQ(report.directions_generated, 7 * c * (c - 1));
+    EXPECT_TRUE(report.condition_a.witness.has_value());
+    if (report.condition_a.witness) {
+        EXPECT_TRUE(tangent_cone_contains(x, *report.condition_a.witness, 1e-9));
+        EXPECT_DOUBLE_EQ(quadratic_form(x, *report.condition_a.witness, s), report.condition_a.witness_value);
+    }
+    // the generic path over materialised directions agrees
+    const auto grad = full_gradient(x, s);
+    const auto dirs = critical_cone_directions(x, grad, cfg);
+    EXPECT_EQ(dirs.size(), report.directions_generated);
+    const auto va = check_condition_a(x, s, dirs, cfg);
+    EXPECT_DOUBLE_EQ(va.witness_value, report.condition_a.witness_value);
+    EXPECT_TRUE(va.witness && *va.witness == *report.condition_a.witness);
+}
+
 int dump() {
     // seven_node goldens: name x0-kind seed method step max_iter restart trace_every
     struct Run { const char* name; InitKind k; std::uint64_t seed; Method m; double step; std::size_t it; bool rs; std::size_t te; };
