@@ -2176,20 +2176,26 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
         const bool work = live && row_fin && C > 1;
         for (int k = pq; k < CP; k += 4) tx[k] = (work && k < C) ? ty[k] : -INFINITY;
         __syncwarp();
-        for (int kk = 2; kk <= CP; kk <<= 1) {
-            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-                for (int i = pq; i < CP; i += 4) {
-                    const int l = i ^ jj;
-                    if (l > i) {
+        // bitonic network over the row copy: each of the 4 lanes takes every 4th
+        // compare-exchange pair of a stage (pair p -> lower index = p with a 0 bit
+        // inserted at log2(jj)), a fixed trip count so the loads pipeline
+        {
+            constexpr int LOGCP = CP == 64 ? 6 : (CP == 128 ? 7 : 8);
+            for (int ks = 1; ks <= LOGCP; ++ks) {
+                for (int js = ks - 1; js >= 0; --js) {
+                    const int jj = 1 << js;
+#pragma unroll 8
+                    for (int t = 0; t < CP / 8; ++t) {
+                        const int pp = pq + 4 * t;
+                        const int i = ((pp >> js) << (js + 1)) | (pp & (jj - 1));
+                        const int l = i | jj;
                         const double a = tx[i], c2 = tx[l];
-                        const bool sw = ((i & kk) == 0) ? (a < c2) : (c2 < a);
-                        if (sw) {
-                            tx[i] = c2;
-                            tx[l] = a;
-                        }
+                        const bool sw = ((i >> ks) & 1) == 0 ? (a < c2) : (c2 < a);
+                        tx[i] = sw ? c2 : a;
+                        tx[l] = sw ? a : c2;
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
         if (pq == 0 && work) {
