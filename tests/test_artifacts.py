@@ -73,3 +73,17 @@ def test_similarity_binary_errors(tmp_path):
     if newc != int(cols[k]):
         with pytest.raises(InvalidInput, match="symmetric|strictly"):
             fc.read_similarity_binary(tmp_path / "y")
+
+
+def test_refine_rng_matches_reference_stream():
+    """api._SplitMix64 (refine's random combinations) == the rng.hpp stream restated in
+    api.splitmix64_stream and the oracle's C splitmix."""
+    from paper_2506_04045_b200 import api
+    for seed in [0, 1, 99, 2**63 + 5]:
+        r = api._SplitMix64(seed)
+        got = [r.next() for _ in range(8)]
+        want = [int(v) for v in api.splitmix64_stream(seed, 0, 8)]
+        assert got == want
+    r = api._SplitMix64(7)
+    d = r.next_double()
+    assert 0.0 <= d < 1.0
