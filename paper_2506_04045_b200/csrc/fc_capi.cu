@@ -947,11 +947,13 @@ bool host_pinned(const void* p) {
 }
 
 // Returns once `src` has been consumed (the DMA may still be in flight, stream-ordered).
-int h2d_big(fc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+// defer_pinned: a page-locked source is only enqueued -- the caller synchronises the
+// stream before it returns to its own caller (the upload overlaps its host work).
+int h2d_big(fc_ctx* ctx, void* dst, const void* src, size_t bytes, bool defer_pinned = false) {
     if (bytes < (size_t(8) << 20)) return h2d(ctx, dst, src, bytes);
     if (host_pinned(src)) {
         CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
+        if (!defer_pinned) CU(cudaStreamSynchronize(ctx->stream));
         return FC_OK;
     }
     TRY(ensure_staging(ctx));
@@ -1271,7 +1273,7 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
     {
         HostPhase hp("row_ptr");
         if (e0 == 0) {                                       // this device's slice starts at entry 0
-            TRY(h2d_big(ctx, ctx->d_row_ptr, row_ptr + r0, (lrow + 1) * sizeof(long long)));
+            TRY(h2d_big(ctx, ctx->d_row_ptr, row_ptr + r0, (lrow + 1) * sizeof(long long), true));
         } else {
             std::vector<long long> rp(lrow + 1);
             for (uint64_t i = 0; i <= lrow; ++i) rp[i] = (long long)(row_ptr[r0 + i] - e0);
@@ -1287,9 +1289,9 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
     } else {
         {
             HostPhase hp("upload col");
-            TRY(h2d_big(ctx, ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t)));
+            TRY(h2d_big(ctx, ctx->d_col, col_idx + e0, lnnz * sizeof(uint32_t), true));
         }
-        if (weighted) TRY(h2d_big(ctx, ctx->d_val, values + e0, lnnz * sizeof(double)));
+        if (weighted) TRY(h2d_big(ctx, ctx->d_val, values + e0, lnnz * sizeof(double), true));
     }
     // node degrees (== column counts, S symmetric) for the hot-row L2 policy
     {
