@@ -676,6 +676,7 @@ int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr) {
     int R = gram_rows_per_chunk(c);
     if (few) R = std::max(R, std::min(128, 4096 / (int)((c + 3) & ~3u)));
     if (TS == 8) R = std::max(8, std::min(16, 2048 / (int)((c + 7) & ~7u)));
+    if (const char* e = std::getenv("FC_GRAM_R")) R = std::max(1, std::min(128, std::atoi(e)));
     const size_t smem = gram_smem((int)c, dual ? 1 : 0, R, TS);
     static PerDevice<size_t[9]> smem_set_pd;
     size_t (&smem_set)[9] = smem_set_pd(ctx);
