@@ -1,0 +1,66 @@
+"""Parity at the benchmark sizes ("live oracle"): the compiled
+reference (oracle/_ref, all host cores) and the device solver run the same FISTA
+iterations on the same bench graph and x0; losses, iteration count, reason and the
+membership must be bit-identical.  Also checks that the device init_membership equals
+the reference's.  Runs on the GPU box (the reference needs ~10-20 s per iteration).
+
+    python scripts/parity_at_scale.py [C] [E128] ...
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import bench
+    import paper_2506_04045_b200 as fc
+    from paper_2506_04045_b200 import capi
+    from oracle import FISTA, GPA, Reference
+    iters = {"A": 100, "B": 5, "C": 3, "E8": 3, "E32": 3, "E64": 2, "E128": 2}
+    ref = Reference()
+    workers = int(ref.lib.fcref_resolve_workers(os.cpu_count() or 1))
+    out = []
+    for name in sys.argv[1:] or ["C"]:
+        cfg = bench.CONFIGS[name]
+        g = bench.make_graph(cfg)
+        k = iters.get(name, 2)
+        method = GPA if cfg["method"] == "gpa" else FISTA
+        t0 = time.perf_counter()
+        x0_ref = ref.init_membership(g.n, cfg["c"], 0, bench.X0_SEED, 0)
+        ctx = capi.Context(0)
+        x0 = fc.init_membership(g.n, cfg["c"], fc.InitStrategy(fc.InitKind.kRandom, bench.X0_SEED), ctx=ctx)
+        same_x0 = x0.tobytes() == x0_ref.tobytes()
+        ctx.upload(g)
+        kw = dict(method=method, max_iter=k, fista_restart=True)
+        ours = ctx.solve(x0, capi.Context.config(**kw))
+        sim = ref.similarity(g, fast=True)
+        t1 = time.perf_counter()
+        want = sim.solve(x0_ref, workers=workers, **kw)
+        t_ref = time.perf_counter() - t1
+        rec_ok = [r[:3] for r in ours["records"]] == [tuple(r[:3]) for r in want["records"]]
+        res = {
+            "config": name, "n": g.n, "nnz": g.nnz, "k": cfg["c"], "method": cfg["method"], "iterations": k,
+            "x0_identical": same_x0,
+            "records_identical": rec_ok,
+            "reason_iterations_identical": (ours["reason"], ours["iterations"]) == (want["reason"], want["iterations"]),
+            "final_loss_identical": ours["final_loss"] == want["final_loss"],
+            "membership_identical": ours["membership"].tobytes() == want["membership"].tobytes(),
+            "max_abs_diff": float(np.max(np.abs(ours["membership"] - want["membership"]))),
+            "losses": [r[1] for r in want["records"]],
+            "reference_workers": workers, "reference_s": round(t_ref, 1), "total_s": round(time.perf_counter() - t0, 1),
+        }
+        print(json.dumps(res), flush=True)
+        out.append(res)
+        ctx.close()
+        del sim
+    return 0 if all(r["membership_identical"] and r["records_identical"] for r in out) else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
