@@ -354,3 +354,31 @@ def test_many_block_gram_tiles_bitwise(oracle, c):
         assert t.share_matrix(x0).tobytes() == oracle.share_matrix(x0).tobytes()
     finally:
         t.close()
+
+
+# ---- live reference at a benchmark size (config B's graph) ------------------------------------
+def test_config_b_graph_bitwise_vs_compiled_reference(reference):
+    """1e6 nodes / 4.1e7 nonzeros (bench config B): the device solver and the compiled
+    reference (all host cores) from the same x0; scripts/parity_at_scale.py does the
+    same for configs A, C and E8-E128 (profiles/r01/parity_at_scale.jsonl)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    g = bench.make_graph(bench.CONFIGS["B"])
+    x0_ref = reference.init_membership(g.n, 16, 0, 1, 0)
+    t = capi.Context(0)
+    try:
+        x0 = fc.init_membership(g.n, 16, fc.InitStrategy(fc.InitKind.kRandom, 1), ctx=t)
+        assert x0.tobytes() == x0_ref.tobytes()
+        t.upload(g)
+        got = t.solve(x0, cfg(method=FISTA, max_iter=3, fista_restart=True))
+    finally:
+        t.close()
+    workers = int(reference.lib.fcref_resolve_workers(os.cpu_count() or 1))
+    want = reference.similarity(g, fast=True).solve(x0_ref, method=FISTA, max_iter=3, fista_restart=True,
+                                                    workers=workers)
+    assert [r[:3] for r in got["records"]] == [tuple(r[:3]) for r in want["records"]]
+    assert (got["reason"], got["iterations"], got["final_loss"]) == (want["reason"], want["iterations"],
+                                                                    want["final_loss"])
+    assert got["membership"].tobytes() == want["membership"].tobytes()
