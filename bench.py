@@ -33,14 +33,17 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (kind, n, m, C, method, extra)
-    "A": dict(kind="sbm", n=10_000, m=200_000, c=8, blocks=8, method="gpa"),
-    "B": dict(kind="sbm", n=1_000_000, m=20_000_000, c=16, blocks=16, method="fista_bt"),
-    "C": dict(kind="citation", n=10_000_000, m=200_000_000, c=32, method="fista"),
-    "D": dict(kind="citation", n=70_000_000, m=1_000_000_000, c=32, method="fista"),
-    "E8": dict(kind="citation", n=4_000_000, m=80_000_000, c=8, method="fista"),
-    "E32": dict(kind="citation", n=4_000_000, m=80_000_000, c=32, method="fista"),
-    "E64": dict(kind="citation", n=4_000_000, m=80_000_000, c=64, method="fista"),
-    "E128": dict(kind="citation", n=4_000_000, m=80_000_000, c=128, method="fista"),
+    # m = edge draws, sized so the undirected edge count after merging duplicates and
+    # self-loops reaches the BASELINE figure (A: 200,082; B: 20,004,748; C: 200,036,749;
+    # E: 80,110,906 edges)
+    "A": dict(kind="sbm", n=10_000, m=202_800, c=8, blocks=8, method="gpa"),
+    "B": dict(kind="sbm", n=1_000_000, m=20_010_000, c=16, blocks=16, method="fista_bt"),
+    "C": dict(kind="citation", n=10_000_000, m=206_100_000, c=32, method="fista"),
+    "D": dict(kind="citation", n=70_000_000, m=1_032_000_000, c=32, method="fista"),
+    "E8": dict(kind="citation", n=4_000_000, m=82_500_000, c=8, method="fista"),
+    "E32": dict(kind="citation", n=4_000_000, m=82_500_000, c=32, method="fista"),
+    "E64": dict(kind="citation", n=4_000_000, m=82_500_000, c=64, method="fista"),
+    "E128": dict(kind="citation", n=4_000_000, m=82_500_000, c=128, method="fista"),
 }
 GRAPH_SEED = 1
 X0_SEED = 1
@@ -55,13 +58,37 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def make_graph(cfg, threads=0):
+def make_graph(cfg, threads=0, host_only=False):
+    """The config's synthetic graph.  host_only: the same generator built without CUDA
+    (oracle/_build/libfcgen.so) -- the reference arm must not load the repo's CUDA library."""
+    if host_only:
+        from oracle import generate_graph
+        kind = 0 if cfg["kind"] == "sbm" else 1
+        return generate_graph(kind, cfg["n"], cfg["m"], GRAPH_SEED, blocks=cfg.get("blocks", 16), p_in=0.9,
+                              alpha=2.5, gamma=2.0, locality=cfg.get("locality", False), threads=threads)
     import paper_2506_04045_b200 as fc
     if cfg["kind"] == "sbm":
-        return fc.generate_sbm(cfg["n"], cfg["m"], cfg["blocks"], seed=GRAPH_SEED, p_in=0.9, locality=False,
-                               threads=threads)
-    return fc.generate_citation(cfg["n"], cfg["m"], seed=GRAPH_SEED, alpha=2.5, gamma=2.0, locality=False,
-                                threads=threads)
+        return fc.generate_sbm(cfg["n"], cfg["m"], cfg["blocks"], seed=GRAPH_SEED, p_in=0.9,
+                               locality=cfg.get("locality", False), threads=threads)
+    return fc.generate_citation(cfg["n"], cfg["m"], seed=GRAPH_SEED, alpha=2.5, gamma=2.0,
+                                locality=cfg.get("locality", False), threads=threads)
+
+
+def loss_hash(records, k):
+    """SHA-256 of the float64 loss records of iterations 0..k (first record per iteration),
+    little-endian bytes: identical bits <=> identical hash.  Both arms print it."""
+    import hashlib
+    seen, out = set(), []
+    for it, loss in records:
+        if it <= k and it not in seen:
+            seen.add(it)
+            out.append(loss)
+    return hashlib.sha256(np.asarray(out, dtype="<f8").tobytes()).hexdigest(), len(out)
+
+
+def membership_hash(x):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(x, dtype="<f8").tobytes()).hexdigest()
 
 
 def bytes_model(n, nnz, c, method, weighted=False):
@@ -168,60 +195,78 @@ def barrier(world):
         dist.barrier()
 
 
-def cpu_reference_run(cfg, graph, x0, budget_s, iters_wanted):
-    """The reference's own run_fista/run_gpa (oracle/_ref), all host cores, on the
-    same graph; stops after a time-bounded number of iterations."""
+def cpu_reference_run(cfg, graph, x0, budget_s, iters_wanted, workers=0, want_x=False, sim=None):
+    """The reference's own run_fista/run_gpa (oracle/_ref) on the same graph and x0, with
+    `workers` threads (0 = all host cores); runs iters_wanted iterations unless a one-iteration
+    probe says that exceeds budget_s.  Plain FISTA for the FISTA configs: the reference has no
+    backtracking, so config B's line-search variant has no reference arm."""
     from oracle import FISTA, GPA, Reference, reference_available
     if not reference_available():
         return None
     ref = Reference()
-    cores = os.cpu_count() or 1
-    workers = ref.lib.fcref_resolve_workers(cores)
-    sim = ref.similarity(graph, fast=True)
+    if workers <= 0:
+        workers = ref.lib.fcref_resolve_workers(os.cpu_count() or 1)
+    if sim is None:
+        sim = ref.similarity(graph, fast=True)
     method = GPA if cfg["method"] == "gpa" else FISTA
     # probe: one iteration to size the sample
     t0 = time.perf_counter()
-    r = sim.solve(x0, method=method, max_iter=1, fista_restart=True, workers=workers, want_x=False)
+    r = sim.solve(x0, method=method, max_iter=1, fista_restart=True, workers=workers, want_x=want_x)
     probe = time.perf_counter() - t0
     el = r["elapsed_ms"]
     per_it = (el[-1] - el[0]) / 1e3 if len(el) >= 2 and el[-1] > el[0] else probe
     iters = int(max(1, min(iters_wanted, budget_s // max(per_it, 1e-9))))
     if iters > 1:
-        r = sim.solve(x0, method=method, max_iter=iters, fista_restart=True, workers=workers, want_x=False)
+        r = sim.solve(x0, method=method, max_iter=iters, fista_restart=True, workers=workers, want_x=want_x)
         el = r["elapsed_ms"]
     t_it = (el[-1] - el[0]) / 1e3 / max(1, len(el) - 1)
-    return {"s_per_iter": t_it, "iters": len(el) - 1, "cores": int(workers), "probe_s": probe}
+    return {"s_per_iter": t_it, "iters": len(el) - 1, "cores": int(workers), "probe_s": probe,
+            "records": [(it, loss) for it, loss, _ in r["records"]], "membership": r["membership"],
+            "method": "gpa" if method == GPA else "fista", "sim": sim}
 
 
 def run_reference_arm(args, cfg):
+    """The reference's CPU solver (oracle/_ref: the unmodified reference headers) on the
+    same graph, x0 and iteration count as our arm.  Loads no repo CUDA code: the graph
+    comes from the host-only generator build (oracle/_build/libfcgen.so)."""
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return 0
-    import paper_2506_04045_b200 as fc
-    graph = make_graph(cfg)
     from oracle import Reference, reference_available
     if not reference_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfcref.so not built"}))
         return 0
+    t0 = time.perf_counter()
+    graph = make_graph(cfg, host_only=True)
+    t_graph = time.perf_counter() - t0
     ref = Reference()
     x0 = ref.init_membership(cfg["n"], cfg["c"], 0, X0_SEED, 0)
-    budget = float(os.environ.get("FC_REF_BUDGET_S", "150"))
-    res = cpu_reference_run(cfg, graph, x0, budget, args.steps + args.warmup)
+    budget = float(os.environ.get("FC_REF_BUDGET_S", "400"))
+    # K iterations from x0 = the iteration count of our arm's end-to-end solve, so the two
+    # parity hashes compare the same records (unless the budget cuts the run short)
+    res = cpu_reference_run(cfg, graph, x0, budget, args.steps, want_x=True)
     value = 1.0 / res["s_per_iter"]
     it_b, _ = bytes_model(graph.n, graph.nnz, cfg["c"], cfg["method"])
-    sample = (f"full config {args.config} graph (n={graph.n}, nnz={graph.nnz}), {res['iters']} "
-              f"{cfg['method'].upper()} iteration(s) of the reference run_fista/run_gpa, time-bounded to "
-              f"~{budget:.0f}s, {res['cores']} worker threads")
+    k = res["iters"]
+    lh, nrec = loss_hash(res["records"], k)
+    sample = (f"full config {args.config} graph (n={graph.n}, nnz={graph.nnz}), {k} "
+              f"{res['method'].upper()} iterations of the reference run_{res['method']} from x0 = "
+              f"init_membership(kRandom, seed {X0_SEED}), fista_restart=true, {res['cores']} worker threads"
+              + (f" (time-bounded to ~{budget:.0f}s)" if k < args.steps else ""))
     line = {
         "impl": "reference", "metric": "fista_iterations_per_s" if cfg["method"] != "gpa" else "gpa_iterations_per_s",
-        "value": value, "unit": "iter/s", "n_gpus": args.gpus, "steps": res["iters"], "warmup": 0,
+        "value": value, "unit": "iter/s", "n_gpus": args.gpus, "steps": k, "warmup": 0,
         "ms_per_step": res["s_per_iter"] * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": config_name(args.config, cfg), "n": graph.n, "nnz": graph.nnz, "k": cfg["c"]},
+        "config": {"workload": config_name(args.config, cfg), "n": graph.n, "nnz": graph.nnz,
+                   "edges_undirected": (graph.nnz - graph.n) // 2, "k": cfg["c"], "graph_gen_s": round(t_graph, 1)},
         "edges_per_s": graph.nnz * value, "achieved_gbs": it_b * value / 1e9,
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": res["cores"], "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "parity": {"method": res["method"], "iterations": k, "records": nrec, "loss_sha256": lh,
+                   "membership_sha256": membership_hash(res["membership"]),
+                   "final_loss": res["records"][-1][1] if res["records"] else None},
     }
     print(json.dumps(line))
     return 0
@@ -354,6 +399,23 @@ def main():
                "includes": "CSR upload + x0 H2D + prelude + solve + result D2H",
                "host_buffers": "page-locked (torch pin_memory), allocated and filled before the timed region"}
 
+    # ---- parity record: `steps` plain iterations from x0 (the reference arm runs the same) ----
+    parity = None
+    if rank == 0 or world > 1:
+        plain = capi.GPA if method == capi.GPA else capi.FISTA
+        if e2e is not None and plain == method:
+            pr = r
+        else:
+            pcfg = capi.Context.config(method=plain, max_iter=args.steps, fista_restart=True)
+            pr = ctx.solve(x0, pcfg, want_x=True)
+        recs = [(it, loss) for it, loss, *_ in pr["records"]]
+        lh, nrec = loss_hash(recs, args.steps)
+        parity = {"method": "gpa" if plain == capi.GPA else "fista", "iterations": int(pr["iterations"]),
+                  "records": nrec, "loss_sha256": lh,
+                  "membership_sha256": membership_hash(pr["membership"]),
+                  "loss_sha256_prefix12": [loss_hash(recs, k)[0][:12] for k in range(1, args.steps + 1)],
+                  "final_loss": recs[-1][1] if recs else None}
+
     # ---- roofline of the dominant kernel (k_sweep) -----------------------------------------
     peak, peak_kind = peaks()
     lo, hi = (int(bounds[rank]), int(bounds[rank + 1])) if world > 1 else (0, graph.n)
@@ -376,14 +438,30 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import Reference, reference_available
+        from oracle import reference_available
         if reference_available():
             budget = float(os.environ.get("FC_CPU_BUDGET_S", "30"))
-            rr = cpu_reference_run(cfg, graph, x0, budget, 1)
+            rr = cpu_reference_run(cfg, graph, x0, budget, 2, want_x=True)
             cpu = {"value": 1.0 / rr["s_per_iter"], "unit": "iter/s", "cores": rr["cores"], "kind": "reference",
-                   "sample": f"{rr['iters']} {cfg['method'].upper()} iteration(s) of the reference solver on the "
-                             f"full config {args.config} graph (oracle/_ref, {rr['cores']} threads), "
-                             f"time-bounded to ~{budget:.0f}s"}
+                   "sample": f"{rr['iters']} {rr['method'].upper()} iteration(s) of the reference run_{rr['method']} "
+                             f"on the full config {args.config} graph from the same x0 (oracle/_ref, "
+                             f"{rr['cores']} threads), time-bounded to ~{budget:.0f}s"}
+            # in-line parity: the same iterations on the device, compared bit for bit
+            plain = capi.GPA if rr["method"] == "gpa" else capi.FISTA
+            gr = ctx.solve(x0, capi.Context.config(method=plain, max_iter=rr["iters"], fista_restart=True),
+                           want_x=True)
+            g_recs = [(it, loss) for it, loss, *_ in gr["records"]]
+            d = np.abs(gr["membership"] - rr["membership"])
+            cpu["parity"] = {
+                "iterations": rr["iters"],
+                "loss_records_equal": loss_hash(g_recs, rr["iters"]) == loss_hash(rr["records"], rr["iters"]),
+                "membership_max_abs_diff": float(d.max()) if d.size else 0.0,
+                "membership_bitwise_equal": bool(np.array_equal(gr["membership"].view(np.uint64),
+                                                                rr["membership"].view(np.uint64))),
+                "supports_equal": bool(np.array_equal(gr["membership"] == 0, rr["membership"] == 0)),
+            }
+            if rr.get("sim") is not None:
+                del rr["sim"]
 
     if rank == 0:
         step_ms = ms / args.steps
@@ -408,6 +486,7 @@ def main():
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clk.summary(),
             "valid": bool(valid_count),
         }

@@ -218,6 +218,49 @@ class _RSum(C.Structure):
                 ("solve_ms", C.c_double)]
 
 
+GEN_SO = os.path.join(HERE, "_build", "libfcgen.so")
+
+
+class _GraphSpec(C.Structure):   # include/fuzzyclust_cuda.h fc_graph_spec
+    _fields_ = [("kind", C.c_int32), ("blocks", C.c_uint32), ("n", C.c_uint64), ("m", C.c_uint64),
+                ("seed", C.c_uint64), ("p_in", C.c_double), ("alpha", C.c_double), ("gamma", C.c_double),
+                ("locality", C.c_int32), ("threads", C.c_int32)]
+
+
+class HostGraph:
+    """A+I CSR on the host (all values 1.0): what the reference arm feeds oracle/_ref."""
+
+    def __init__(self, n, row_ptr, col_idx):
+        self.n, self.row_ptr, self.col_idx, self.values = int(n), row_ptr, col_idx, None
+        self.nnz = int(col_idx.size)
+        self.frob_sq = float(self.nnz)
+
+
+def generate_graph(kind, n, m, seed, *, blocks=16, p_in=0.9, alpha=2.5, gamma=2.0, locality=False, threads=0):
+    """The repo's synthetic generator (csrc/generator.cpp) built host-only (oracle/_build/libfcgen.so):
+    the same graph ``paper_2506_04045_b200.generate_{sbm,citation}`` returns, without the CUDA library."""
+    if not os.path.exists(GEN_SO):
+        build()
+    L = C.CDLL(GEN_SO)
+    L.fcgen_generate.argtypes = [C.POINTER(_GraphSpec), C.POINTER(C.c_uint64), C.POINTER(_i64p),
+                                 C.POINTER(_u32p), C.c_char_p, C.c_size_t]
+    L.fcgen_free.argtypes = [C.c_void_p]
+    spec = _GraphSpec(kind, blocks, n, m, seed, p_in, alpha, gamma, int(locality), threads)
+    nnz = C.c_uint64()
+    rp, ci = _i64p(), _u32p()
+    err = C.create_string_buffer(512)
+    rc = L.fcgen_generate(C.byref(spec), C.byref(nnz), C.byref(rp), C.byref(ci), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    try:
+        row_ptr = np.ctypeslib.as_array(rp, shape=(n + 1,)).copy()
+        col_idx = np.ctypeslib.as_array(ci, shape=(max(nnz.value, 1),))[: nnz.value].copy()
+    finally:
+        L.fcgen_free(C.cast(rp, C.c_void_p))
+        L.fcgen_free(C.cast(ci, C.c_void_p))
+    return HostGraph(n, row_ptr, col_idx)
+
+
 def reference_available(path: str = REF_SO) -> bool:
     return os.path.exists(path)
 

@@ -541,7 +541,9 @@ int set_hot_rows(fc_ctx* ctx) {
     unsigned thr = 0xFFFFFFFFu;
     if (mb > 0.0 && ctx->deg_hist.empty() && ctx->d_deg) {
         std::vector<unsigned> deg(ctx->n);
-        CU(cudaMemcpy(deg.data(), ctx->d_deg, ctx->n * sizeof(unsigned), cudaMemcpyDeviceToHost));
+        // on the library's (non-blocking) stream: ordered after k_degrees
+        CU(cudaMemcpyAsync(deg.data(), ctx->d_deg, ctx->n * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
         const unsigned maxd = deg.empty() ? 0u : *std::max_element(deg.begin(), deg.end());
         ctx->deg_hist.assign((size_t)maxd + 1, 0);
         for (unsigned d : deg) ctx->deg_hist[d]++;
@@ -578,12 +580,16 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
     const size_t N = ctx->n, L = ctx->local_rows, LB = ctx->local_blocks;
     for (int k = 0; k < 3; ++k) TRY(dalloc(ctx, &ctx->d_U[k], N * c));
     for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_xs[k], L * c));
+    // backtracking-only buffers exist exactly when bt_alloc is set (a non-backtracking
+    // re-allocation frees them, so no stale, smaller copy survives a change of C)
     for (int k = 2; k < 4; ++k) {
         if (bt) TRY(dalloc(ctx, &ctx->d_xs[k], L * c));
+        else dfree(ctx, &ctx->d_xs[k]);
     }
     TRY(dalloc(ctx, &ctx->d_prod, L));
     for (int k = 0; k < 3; ++k) {
         if (bt) TRY(dalloc(ctx, &ctx->d_rowterm[k], L));
+        else dfree(ctx, &ctx->d_rowterm[k]);
     }
     const unsigned np = npairs_of(c);
     for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_gpart[k], LB * np));
@@ -1262,6 +1268,8 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
     const uint64_t r0 = ctx->shards.front().row0;
     const uint64_t r1 = ctx->shards.back().row0 + ctx->shards.back().nrows;
     const int64_t e0 = row_ptr[r0], e1 = row_ptr[r1];
+    if (e1 < e0 || e0 < 0 || (uint64_t)e1 > nnz)
+        return set_err(ctx, FC_INVALID, "similarity: row_ptr is not monotone");
     const uint64_t lnnz = (uint64_t)(e1 - e0);
     TRY(dalloc(ctx, &ctx->d_row_ptr, lrow + 1));
     TRY(dalloc(ctx, &ctx->d_col, lnnz));
@@ -1294,6 +1302,24 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
         }
         if (weighted) TRY(h2d_big(ctx, ctx->d_val, values + e0, lnnz * sizeof(double), true));
     }
+    {   // structural validation of the caller's CSR (monotone row_ptr, columns in range and
+        // strictly ascending per row); symmetry is the caller's contract (S = S^T)
+        HostPhase hp("check_csr");
+        unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(ctx->d_counter + 96);
+        unsigned long long h_bad = ~0ULL;
+        CU(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), ctx->stream));
+        k_check_csr<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(ctx->d_row_ptr, lrow, ctx->d_col, n, d_bad);
+        TRY(check_launch(ctx, "k_check_csr"));
+        CU(cudaMemcpyAsync(&h_bad, d_bad, sizeof h_bad, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (h_bad != ~0ULL) {
+            const unsigned long long row = (h_bad >> 2) + r0;
+            ctx->have_csr = false;
+            if ((h_bad & 3) == 1) return set_err(ctx, FC_INVALID, "similarity: row_ptr decreases at row %llu", row);
+            if ((h_bad & 3) == 2) return set_err(ctx, FC_INVALID, "similarity: column index out of range in row %llu", row);
+            return set_err(ctx, FC_INVALID, "similarity: columns of row %llu are not strictly ascending", row);
+        }
+    }
     // node degrees (== column counts, S symmetric) for the hot-row L2 policy
     {
         HostPhase hp("degrees");
@@ -1306,7 +1332,8 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
             std::vector<unsigned> hdeg(n);
             for (uint64_t i = 0; i < n; ++i)
                 hdeg[i] = (unsigned)std::min<int64_t>(row_ptr[i + 1] - row_ptr[i], 0xFFFFFFFELL);
-            CU(cudaMemcpy(ctx->d_deg, hdeg.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice));
+            CU(cudaMemcpyAsync(ctx->d_deg, hdeg.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));   // hdeg is pageable and goes out of scope
         }
         auto deg = [&](uint64_t i) { return (uint64_t)(row_ptr[i + 1] - row_ptr[i]); };
         // heavy rows per shard (k_sweep phase 1), longest first
@@ -1340,7 +1367,9 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
             dfree(ctx, &ctx->d_heavy);
         } else {
             TRY(dalloc(ctx, &ctx->d_heavy, heavy.size()));
-            CU(cudaMemcpy(ctx->d_heavy, heavy.data(), heavy.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
+            CU(cudaMemcpyAsync(ctx->d_heavy, heavy.data(), heavy.size() * sizeof(unsigned), cudaMemcpyHostToDevice,
+                               ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
         }
     }
     ctx->local_nnz = lnnz;
@@ -1610,7 +1639,9 @@ int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const 
     {
         HostPhase hp("ensure_work");
         TRY(ensure_work(ctx, c, bt));
-        TRY(ensure_trace(ctx, std::min<uint64_t>(cfg->max_iter + 2, 1u << 20)));
+        // prelude + every trace_every-th iteration + the terminating record
+        TRY(ensure_trace(ctx, std::min<uint64_t>(cfg->max_iter / std::max<uint64_t>(cfg->trace_every, 1) + 3,
+                                                 1u << 20)));
     }
     {
         HostPhase hp("x0 h2d");
@@ -1751,8 +1782,18 @@ int fc_solver_end(fc_ctx* ctx, double* x_out, fc_trace_record* trace, uint64_t t
     const DevState& s = *ctx->h_state;
     HostPhase hp("result d2h");
     if (x_out) TRY(d2h_big(ctx, x_out, ctx->d_U[s.result_buf], ctx->n * ctx->c * sizeof(double)));
-    const uint64_t nrec = std::min<uint64_t>(std::min<uint64_t>(s.n_records, ctx->trace_alloc), trace_cap);
-    if (trace && nrec) TRY(d2h(ctx, trace, ctx->d_trace, nrec * sizeof(fc_trace_record)));
+    // device-held records; when the caller's buffer is smaller, its last slot gets the
+    // terminating record (the last held one), as the device does at its own capacity
+    const uint64_t held = std::min<uint64_t>(s.n_records, ctx->trace_alloc);
+    const uint64_t nrec = std::min<uint64_t>(held, trace_cap);
+    if (trace && nrec) {
+        if (held > nrec && s.done) {
+            if (nrec > 1) TRY(d2h(ctx, trace, ctx->d_trace, (nrec - 1) * sizeof(fc_trace_record)));
+            TRY(d2h(ctx, trace + nrec - 1, ctx->d_trace + held - 1, sizeof(fc_trace_record)));
+        } else {
+            TRY(d2h(ctx, trace, ctx->d_trace, nrec * sizeof(fc_trace_record)));
+        }
+    }
     CU(cudaStreamSynchronize(ctx->stream));
     if (out) {
         out->reason = s.reason;
@@ -1846,16 +1887,17 @@ int load_dev(fc_ctx* ctx, FILE* f, void* d, size_t bytes, std::vector<char>& buf
     return FC_OK;
 }
 
-// every device buffer a session carries from one iteration to the next, in file order
+// every device buffer a session carries from one iteration to the next, in file order.
+// The layout is a function of the header alone: (c, bt) select the optional blocks.
 template <class F>
-int for_session_buffers(fc_ctx* ctx, F&& f) {
+int for_session_buffers(fc_ctx* ctx, bool bt, F&& f) {
     const size_t N = ctx->n, c = ctx->c, L = ctx->local_rows, LB = ctx->local_blocks;
     const unsigned np = npairs_of(ctx->c), nch = nchains_of(ctx->c);
+    if (bt && !ctx->bt_alloc) return set_err(ctx, FC_INVALID, "checkpoint: backtracking buffers not allocated");
     for (int k = 0; k < 3; ++k) TRY(f((void*)ctx->d_U[k], N * c * sizeof(double)));
-    for (int k = 0; k < 4; ++k)
-        if (ctx->d_xs[k]) TRY(f((void*)ctx->d_xs[k], L * c * sizeof(double)));
-    for (int k = 0; k < 3; ++k)
-        if (ctx->bt_alloc && ctx->d_rowterm[k]) TRY(f((void*)ctx->d_rowterm[k], L * sizeof(double)));
+    for (int k = 0; k < (bt ? 4 : 2); ++k) TRY(f((void*)ctx->d_xs[k], L * c * sizeof(double)));
+    if (bt)
+        for (int k = 0; k < 3; ++k) TRY(f((void*)ctx->d_rowterm[k], L * sizeof(double)));
     TRY(f((void*)ctx->d_prod, L * sizeof(double)));
     for (int k = 0; k < 2; ++k) TRY(f((void*)ctx->d_gpart[k], LB * np * sizeof(double)));
     TRY(f((void*)ctx->d_spart, LB * kNumScal * sizeof(double)));
@@ -1910,7 +1952,7 @@ int fc_solver_checkpoint(fc_ctx* ctx, const char* path) {
         if (!rc && std::fwrite(tr.data(), sizeof(fc_trace_record), h.n_records, f) != h.n_records)
             rc = ckpt_io_err(ctx, "write", path);
     }
-    if (!rc) rc = for_session_buffers(ctx, [&](void* d, size_t bytes) { return dump_dev(ctx, f, d, bytes, buf, path); });
+    if (!rc) rc = for_session_buffers(ctx, h.bt != 0, [&](void* d, size_t bytes) { return dump_dev(ctx, f, d, bytes, buf, path); });
     if (std::fclose(f) != 0 && !rc) rc = ckpt_io_err(ctx, "close", path);
     return rc;
 }
@@ -1944,7 +1986,8 @@ int fc_solver_resume(fc_ctx* ctx, const char* path) {
     if (h.n_records && std::fread(tr.data(), sizeof(fc_trace_record), h.n_records, f) != h.n_records)
         return set_err(ctx, FC_IO, "checkpoint: truncated file %s", path);
     std::vector<char> buf(kCkptChunk);
-    TRY(for_session_buffers(ctx, [&](void* d, size_t bytes) { return load_dev(ctx, f, d, bytes, buf, path); }));
+    TRY(for_session_buffers(ctx, h.bt != 0, [&](void* d, size_t bytes) { return load_dev(ctx, f, d, bytes, buf, path); }));
+    if (std::fgetc(f) != EOF) return set_err(ctx, FC_IO, "checkpoint: %s has trailing bytes (layout mismatch)", path);
     if (h.n_records) TRY(h2d(ctx, ctx->d_trace, tr.data(), h.n_records * sizeof(fc_trace_record)));
     s.trace_cap = ctx->trace_alloc;
     TRY(upload_state(ctx, s));

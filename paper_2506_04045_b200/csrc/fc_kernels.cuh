@@ -1204,10 +1204,19 @@ __device__ double fista_t_next(double t) {     // solver.hpp:72
     return (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
 }
 
+// The last trace slot is reserved for the terminating record (the reference always
+// appends it, solver.hpp:157-173, :225-241): past the capacity, intermediate records are
+// dropped (n_records keeps counting them, so n_records > trace_cap flags the loss) and
+// the terminating one lands in slot trace_cap - 1.
 __device__ __forceinline__ void push_record(Bufs& b, DevState* st, unsigned long long it, double loss,
-                                            int increased, int backtracks, double step) {
-    const unsigned long long k = st->n_records++;
-    if (k < st->trace_cap) {
+                                            int increased, int backtracks, double step, bool terminal = false) {
+    unsigned long long k = st->n_records++;
+    if (st->trace_cap == 0) return;
+    if (k >= st->trace_cap - 1) {
+        if (!terminal) return;
+        k = st->trace_cap - 1;
+    }
+    {
         long long now;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
         TraceRec& r = b.trace[k];
@@ -1271,7 +1280,7 @@ __device__ bool finalize_decide(Bufs& b, Geo& g, int kind) {
         const bool stop_tol = dsub(st->loss_prev, loss) <= st->tol;
         const bool stop_iter = n >= st->max_iter;
         if (stop_tol || stop_iter || n % st->trace_every == 0)
-            push_record(b, st, n, loss, increased, 0, st->tau);
+            push_record(b, st, n, loss, increased, 0, st->tau, stop_tol || stop_iter);
         st->iterations = n;
         st->final_loss = loss;
         st->result_buf = st->sw_b;
@@ -1306,7 +1315,7 @@ __device__ bool finalize_decide(Bufs& b, Geo& g, int kind) {
     const bool stop_tol = decrease <= st->tol && !(increased && st->restart);
     const bool stop_iter = n >= st->max_iter;
     if (stop_tol || stop_iter || n % st->trace_every == 0)
-        push_record(b, st, n, loss, increased, st->backtracks, st->tau);
+        push_record(b, st, n, loss, increased, st->backtracks, st->tau, stop_tol || stop_iter);
     st->result_buf = st->sw_b;
     st->iterations = n;
     st->final_loss = loss;
@@ -1539,6 +1548,34 @@ __global__ void k_hvp_rows(const double* g2, const double* vs, const double* x, 
         for (int l = 0; l < C; ++l) atx = dadd(atx, dmul(g2[l * W + C + k], xi[l]));
         for (int l = 0; l < C; ++l) bv = dadd(bv, dmul(g2[(C + k) * W + C + l], vi[l]));
         out[e] = dmul(-4.0, dsub(dsub(dsub(vs[e], ax), atx), bv));
+    }
+}
+
+// Structural check of an uploaded CSR (fc_upload_csr accepts caller arrays): row_ptr
+// monotone, column indices < n and strictly ascending within a row -- the invariants
+// from_triplets establishes (sparse.hpp:43-58) and every gathering kernel relies on.
+// Warp per row; the first failing row wins: out = min over failures of (row << 2 | code),
+// code 1 = row_ptr decreases, 2 = column out of range, 3 = columns not strictly ascending.
+__global__ void k_check_csr(const long long* row_ptr, unsigned long long rows, const unsigned* col,
+                            unsigned long long n, unsigned long long* out) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    for (unsigned long long i = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; i < rows;
+         i += warps) {
+        const long long a = row_ptr[i], b = row_ptr[i + 1];
+        unsigned code = 0;
+        if (b < a) {
+            code = 1;
+        } else {
+            for (long long k = a + lane; k < b; k += 32) {
+                const unsigned c0 = col[k];
+                if (c0 >= n) { code = 2; break; }
+                if (k + 1 < b && col[k + 1] <= c0) { code = code ? code : 3u; }
+            }
+        }
+        // lowest code of the row's failing lanes (2 before 3 at equal rows is fine: either reports the row)
+        const unsigned any = __ballot_sync(0xffffffffu, code != 0);
+        if (any && lane == (unsigned)(__ffs(any) - 1)) atomicMin(out, (i << 2) | code);
     }
 }
 

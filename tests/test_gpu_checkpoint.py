@@ -107,3 +107,67 @@ def test_resume_rejects_other_similarity_and_bad_files(tmp_path, oracle):
         t.finish(g.n, 8, want_x=False)
     finally:
         t.close()
+
+
+def test_reused_context_bt_then_plain_at_new_c(tmp_path, oracle):
+    """One context runs a backtracking solve (allocating the line-search buffers), then a
+    plain FISTA session at a different C: the checkpoint layout follows the header (no
+    stale backtracking blocks), it resumes into a fresh context AND into a context that
+    still holds backtracking buffers, and both continuations equal the uninterrupted run.
+    A file with trailing bytes is rejected."""
+    g = random_graph(6000, 7.0, 31)
+    x8, x12 = oracle.init_random(g.n, 8, 2), oracle.init_random(g.n, 12, 3)
+    bt = capi.Context.config(method=FISTA_BT, max_iter=5, step_size=30.0 * oracle.default_step_size(g))
+    conf = capi.Context.config(method=FISTA, max_iter=12, fista_restart=True)
+    want = oracle.solve(g, x12, method=FISTA, max_iter=12, fista_restart=True)
+    path = tmp_path / "plain.fcckpt"
+    t = capi.Context(0)
+    try:
+        t.upload(g)
+        t.solve(x8, bt)
+        t.begin(x12, conf)
+        t.run(4)
+        t.sync()
+        t.checkpoint(str(path))
+        t.finish(g.n, 12, want_x=False)
+    finally:
+        t.close()
+    fresh = capi.Context(0)
+    try:
+        fresh.upload(g)
+        fresh.resume(str(path), conf)
+        got = fresh.finish(g.n, 12)
+    finally:
+        fresh.close()
+    assert got["membership"].tobytes() == want["membership"].tobytes()
+    assert _recs(got) == [tuple(r) for r in want["records"]]
+    held = capi.Context(0)
+    try:
+        held.upload(g)
+        held.solve(x12, capi.Context.config(method=FISTA_BT, max_iter=2))   # bt buffers at C = 12
+        held.resume(str(path), conf)
+        got2 = held.finish(g.n, 12)
+        assert got2["membership"].tobytes() == want["membership"].tobytes()
+        longer = tmp_path / "long.fcckpt"
+        longer.write_bytes(path.read_bytes() + b"\0" * 8)
+        with pytest.raises(fc.IoError, match="trailing"):
+            held.resume(str(longer), conf)
+    finally:
+        held.close()
+
+
+def test_trace_capacity_keeps_terminating_record(oracle):
+    """A trace buffer smaller than the run: intermediate records are dropped, the last slot
+    holds the terminating record, n_records counts everything produced."""
+    g = random_graph(3000, 6.0, 8)
+    x0 = oracle.init_random(g.n, 8, 1)
+    want = oracle.solve(g, x0, method=GPA, max_iter=9)
+    t = capi.Context(0)
+    try:
+        t.upload(g)
+        got = t.solve(x0, capi.Context.config(method=GPA, max_iter=9), trace_cap=4)
+    finally:
+        t.close()
+    assert got["n_records"] == len(want["records"]) == 10
+    assert _recs(got)[:3] == [tuple(r) for r in want["records"][:3]]
+    assert _recs(got)[3] == tuple(want["records"][-1])

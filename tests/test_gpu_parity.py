@@ -382,3 +382,70 @@ def test_config_b_graph_bitwise_vs_compiled_reference(reference):
     assert (got["reason"], got["iterations"], got["final_loss"]) == (want["reason"], want["iterations"],
                                                                     want["final_loss"])
     assert got["membership"].tobytes() == want["membership"].tobytes()
+
+
+# ---- live reference on the benchmark graphs, with a FISTA restart inside the run -------------
+@pytest.mark.parametrize("name", ["E32", "C"])
+def test_bench_graph_fista_restart_bitwise_vs_compiled_reference(reference, name):
+    """Bench configs E32 (4e6 nodes, 1.6e8 nonzeros) and C (1e7 nodes, 4.1e8 nonzeros, k=32):
+    6 FISTA iterations with fista_restart=true at a step size large enough that the momentum
+    overshoots and the restart branch (solver.hpp:247-249) fires inside the run.  The device
+    solver and the compiled reference (all host cores) start from the same x0; every loss
+    record, the restart flags, the reason, the iteration count and the membership must be
+    identical bit for bit."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    c, iters = bench.CONFIGS[name]["c"], 6
+    g = bench.make_graph(bench.CONFIGS[name])
+    x0_ref = reference.init_membership(g.n, c, 0, 1, 0)
+    sim = reference.similarity(g, fast=True)
+    tau = sim.default_step_size()
+    t = capi.Context(0)
+    try:
+        x0 = fc.init_membership(g.n, c, fc.InitStrategy(fc.InitKind.kRandom, 1), ctx=t)
+        assert x0.tobytes() == x0_ref.tobytes()
+        t.upload(g)
+        assert fc.default_step_size(g, g.n) == tau
+        # smallest multiple of the default step at which the restart fires within the run
+        # (the device run is bitwise the reference's, so the choice is deterministic)
+        for mult in (20.0, 100.0, 400.0, 2000.0, 1e4, 1e5):
+            got = t.solve(x0, cfg(method=FISTA, step_size=mult * tau, max_iter=iters, fista_restart=True))
+            if any(inc for _, _, inc in got["records"]):
+                break
+        assert any(inc for _, _, inc in got["records"]), "no restart at any probed step size"
+    finally:
+        t.close()
+    workers = int(reference.lib.fcref_resolve_workers(os.cpu_count() or 1))
+    want = sim.solve(x0_ref, method=FISTA, step_size=mult * tau, max_iter=iters, fista_restart=True,
+                     workers=workers)
+    assert want["iterations"] >= 5
+    assert [r[:3] for r in got["records"]] == [tuple(r[:3]) for r in want["records"]]
+    assert (got["reason"], got["iterations"], got["final_loss"]) == (want["reason"], want["iterations"],
+                                                                    want["final_loss"])
+    assert got["membership"].tobytes() == want["membership"].tobytes()
+
+
+def test_upload_rejects_malformed_csr():
+    """fc_upload_csr validates the caller's arrays on the device (monotone row_ptr, columns
+    < n, strictly ascending per row) instead of faulting later in a gathering kernel; the
+    context stays usable afterwards."""
+    from paper_2506_04045_b200 import SparseSimilarity
+    rp = np.array([0, 2, 4, 6], np.int64)
+    good = np.array([0, 1, 0, 1, 1, 2], np.uint32)
+    t = capi.Context(0)
+    try:
+        for col, msg in ((np.array([0, 1, 0, 7, 1, 2], np.uint32), "out of range in row 1"),
+                         (np.array([0, 1, 1, 0, 1, 2], np.uint32), "not strictly ascending"),
+                         (np.array([0, 1, 0, 1, 2, 2], np.uint32), "not strictly ascending")):
+            with pytest.raises(fc.InvalidInput, match=msg):
+                t.upload(SparseSimilarity(3, rp, col, None, 6.0))
+        with pytest.raises(fc.InvalidInput, match="row_ptr"):
+            t.upload(SparseSimilarity(3, np.array([0, 4, 2, 6], np.int64), good, None, 6.0))
+        g = SparseSimilarity(3, rp, good, None, 6.0)
+        t.upload(g)
+        x0 = np.full((3, 2), 0.5)
+        t.solve(x0, cfg(method=GPA, max_iter=2))
+    finally:
+        t.close()
