@@ -280,6 +280,7 @@ class Reference:
         L.fcref_similarity_nnz.restype = C.c_uint64
         L.fcref_similarity_nnz.argtypes = [C.c_void_p]
         L.fcref_similarity_export.argtypes = [C.c_void_p, _i64p, _u32p, _dp]
+        L.fcref_from_triplets.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _dp, C.POINTER(C.c_void_p)]
         L.fcref_build_similarity.argtypes = [C.c_uint64, C.c_uint64, _u32p, C.POINTER(C.c_void_p)]
         L.fcref_project_simplex.argtypes = [_dp, C.c_uint64]
         L.fcref_splitmix.restype = C.c_uint64
@@ -318,6 +319,16 @@ class Reference:
         self._check(self.lib.fcref_similarity_create(graph.n, graph.nnz, _ptr(graph.row_ptr, _i64p),
                                                      _ptr(graph.col_idx, _u32p), _ptr(graph.values),
                                                      int(fast), C.byref(h)))
+        return RefSimilarity(self, h)
+
+    def from_triplets(self, n, rows, cols, values):
+        """sparse.hpp:28-62 on triplets in the given order (uint32 indices, float64 values)."""
+        r = np.ascontiguousarray(rows, dtype=np.uint32)
+        c = np.ascontiguousarray(cols, dtype=np.uint32)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        h = C.c_void_p()
+        self._check(self.lib.fcref_from_triplets(n, r.size, _ptr(r, _u32p), _ptr(c, _u32p), _ptr(v),
+                                                 C.byref(h)))
         return RefSimilarity(self, h)
 
     def build_similarity(self, num_nodes, edges):

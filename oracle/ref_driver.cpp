@@ -129,6 +129,19 @@ int fcref_similarity_create(uint64_t n, uint64_t nnz, const int64_t* row_ptr, co
     });
 }
 
+// SparseSimilarity::from_triplets (sparse.hpp:28-62) on raw triplets in caller order
+// (unsorted, possibly invalid): pins the device construction, messages included.
+int fcref_from_triplets(uint64_t n, uint64_t count, const uint32_t* rows, const uint32_t* cols,
+                        const double* values, void** out) {
+    return guarded([&] {
+        std::vector<std::tuple<std::uint32_t, std::uint32_t, double>> t;
+        t.reserve(count);
+        for (uint64_t k = 0; k < count; ++k) t.emplace_back(rows[k], cols[k], values[k]);
+        auto* s = new SparseSimilarity(SparseSimilarity::from_triplets(n, std::move(t)));
+        *out = s;
+    });
+}
+
 void fcref_similarity_free(void* s) { delete static_cast<SparseSimilarity*>(s); }
 double fcref_similarity_frob_sq(void* s) { return static_cast<SparseSimilarity*>(s)->frob_sq(); }
 uint64_t fcref_similarity_nnz(void* s) { return static_cast<SparseSimilarity*>(s)->nnz(); }

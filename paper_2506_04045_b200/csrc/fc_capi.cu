@@ -153,6 +153,7 @@ struct fc_ctx {
     bool sweep_tma = false;            // FC_SWEEP=tma selects the TMA gather4 sweep
     bool sweep_groups = false;       // FC_SWEEP=groups: per-group row sweep for C <= 16
     bool step_big = false;             // FC_STEP=big: thread-per-row k_step_big for C > 32
+    bool fuse_gram = true;             // FC_FUSE=0: separate k_step_t + k_gram for C <= 32 FISTA
     bool umaps_ok = false;
     UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
 
@@ -399,6 +400,33 @@ int launch_step_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_t launch: %s", cudaGetErrorString(e));
     return FC_OK;
 }
+
+template <int G, bool EXACT>
+int launch_step_gram(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
+    const size_t smem = step_t_smem(G);
+    if (!grid) {
+        CU(cudaFuncSetAttribute(k_step_gram<G, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_gram<G, EXACT>, kStepThreads, smem, ctx->sm_count);
+    }
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, g.nblk));
+    k_step_gram<G, EXACT><<<gr, kStepThreads, smem, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_gram launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
+template <int G, int S>
+struct LaunchStepGram {
+    static int run(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+        if (g.nrows == 0) return FC_OK;
+        if constexpr (S == 1)
+            return g.C == (unsigned)G ? launch_step_gram<G, true>(ctx, b, g) : launch_step_gram<G, false>(ctx, b, g);
+        return set_err(ctx, FC_INVALID, "k_step_gram: C > 32");
+    }
+};
 
 template <int CP>
 int launch_step_big(fc_ctx* ctx, const Bufs& b, const Geo& g) {
@@ -664,6 +692,19 @@ int phase_step(fc_ctx* ctx, int bt) {
     return FC_OK;
 }
 
+// FISTA step + the dual Gram of the new iterate in one pass (C <= 32, no backtracking)
+bool fused_step_gram(const fc_ctx* ctx, int bt) { return ctx->fuse_gram && !bt && ctx->c <= 32; }
+
+int phase_step_gram(fc_ctx* ctx) {
+    ProfScope p(ctx, kClsStep);
+    for (size_t s = 0; s < ctx->shards.size(); ++s) {
+        const Bufs b = make_bufs(ctx, s);
+        const Geo g = make_geo(ctx, s);
+        TRY(by_c<LaunchStepGram>(ctx, ctx->c, ctx, b, g));
+    }
+    return FC_OK;
+}
+
 int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr) {
     if (!strm) strm = ctx->stream;
     ProfScope p(ctx, kClsGram);
@@ -818,9 +859,15 @@ static int gram_and_sweep(fc_ctx* ctx) {
 }
 
 int enqueue_fista_iteration(fc_ctx* ctx, int bt) {
-    TRY(phase_step(ctx, bt));
-    TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
-    TRY(gram_and_sweep(ctx));
+    if (fused_step_gram(ctx, bt)) {
+        TRY(phase_step_gram(ctx));
+        TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
+        TRY(phase_sweep(ctx, true));
+    } else {
+        TRY(phase_step(ctx, bt));
+        TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
+        TRY(gram_and_sweep(ctx));
+    }
     TRY(phase_rowsum(ctx, bt));
     TRY(phase_combine(ctx, 3, bt ? 0xF : 1));
     TRY(phase_finalize(ctx, kFinFista, 3));
@@ -1116,6 +1163,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         ctx->sweep_groups = std::strcmp(sw, "groups") == 0;
     }
     if (const char* sp = std::getenv("FC_STEP")) ctx->step_big = std::strcmp(sp, "big") == 0;
+    if (const char* fu = std::getenv("FC_FUSE")) ctx->fuse_gram = std::strcmp(fu, "0") != 0;
     if (const char* gr = std::getenv("FC_GRAPHS")) ctx->graphs = std::strcmp(gr, "0") != 0;
     {
         const unsigned hw = std::thread::hardware_concurrency();

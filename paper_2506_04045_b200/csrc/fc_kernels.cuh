@@ -1743,143 +1743,285 @@ __device__ __forceinline__ void fold_residual(double (&w)[CP], int C) {
 // G (power of two, 2..32) is the padded row width, C <= G; EXACT: C == G.
 constexpr int kStepThreads = 128;
 
+// Per-kernel invariants of a k_step_t / k_step_gram batch (read from the plan once).
+struct StepPlan {
+    const double* A;                                         // bar^{n-1} (or the literal point)
+    const double* Bp;                                        // bar^{n-2}
+    double* D;                                               // receives bar^n
+    const double* XS;                                        // S X_ext^n (or S bar)
+    double beta, tau;
+    int mode;
+};
+
+__device__ __forceinline__ StepPlan step_plan(const Bufs& b) {
+    const DevState* st = b.st;
+    StepPlan p;
+    p.mode = st->step_mode;
+    p.A = b.U[st->step_a];
+    p.Bp = b.U[st->step_b];
+    p.D = b.U[st->step_dst];
+    p.beta = st->beta_step;
+    p.tau = st->tau;
+    p.XS = b.xs[st->xs_r * 2 + st->step_sel];
+    return p;
+}
+
+// Gr[k*G + l] = G[k][l] (zero padded to G x G) from the expanded C x C matrix of the plan.
+template <int G>
+__device__ __forceinline__ void stage_gram_matrix(const Bufs& b, double* Gr, int C) {
+    const double* __restrict__ Gt = b.gfull[b.st->step_sel];   // Gt[l*C + k] == G[k][l]
+    for (int e = threadIdx.x; e < G * G; e += blockDim.x) {
+        const int k = e / G, l = e % G;
+        Gr[e] = (k < C && l < C) ? Gt[l * C + k] : 0.0;
+    }
+}
+
+// One warp, rows [rb, min(rb + 32, rend)) of the shard: the K3 batch described above.
+// Tiles TA/TB/TX are the warp's [32][G+1]; on return TA holds the A rows (bar^{n-1})
+// and TX the new rows bar^n (already stored to D).  Returns false on a non-finite y.
 // BT: also the backtracking row terms (as k_step): lin_i = sum_r g_r (bar_r - x_r),
 // sq_i = sum_r (bar_r - x_r)^2, <xs_i, x_i>; g is parked in the thread's A-tile row.
+template <int G, bool EXACT, bool BT>
+__device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, const Geo& g, const double* Gr,
+                                             int C, double* TA, double* TB, double* TX, unsigned long long rb,
+                                             unsigned long long rend) {
+    constexpr int LD = G + 1;
+    constexpr int RPW = 32 / G;
+    constexpr int KU = G < 4 ? G : 4;
+    const unsigned lane = threadIdx.x & 31u;
+    const int lg = (int)(lane % G);
+    const int sub = (int)(lane / G);
+    const bool lane_ok = EXACT || lg < C;
+    const int mode = sp.mode;
+    const double* __restrict__ A = sp.A;
+    const double* __restrict__ Bp = sp.Bp;
+    const double* __restrict__ XS = sp.XS;
+    double* ra = TA + lane * LD;                             // this thread's row in phase 2
+    const double* rb_ = TB + lane * LD;
+    double* tr = TX + lane * LD;
+    bool bad = false;
+    const bool row_ok = rb + lane < rend;
+    // 1: async loads of the batch
+    for (int p = 0; p < 32; p += RPW) {
+        const unsigned long long row = rb + p + sub;
+        if (row < rend && lane_ok) {
+            const size_t a = (size_t)(g.row0 + row) * C + lg;
+            const int t = (p + sub) * LD + lg;
+            cp_async8(TA + t, A + a);
+            if (mode != kLiteral) cp_async8(TB + t, Bp + a);
+            cp_async8(TX + t, XS + (size_t)row * C + lg);
+        }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    if (row_ok) {
+        double xr[G];
+#pragma unroll
+        for (int l = 0; l < G; ++l)
+            xr[l] = (EXACT || l < C) ? ((mode == kLiteral) ? ra[l] : extrap(ra[l], rb_[l], sp.beta)) : 0.0;
+        double mi = 0.0;                                     // BT: <xs_i, x_i>, component order
+        if constexpr (BT) {
+#pragma unroll
+            for (int k = 0; k < G; ++k)
+                if (EXACT || k < C) mi = dadd(mi, dmul(tr[k], xr[k]));
+        }
+        // gradient (objective.hpp:37-43, :116-117), KU independent chains
+#pragma unroll 1
+        for (int k0 = 0; k0 < C; k0 += KU) {
+            double o[KU];
+#pragma unroll
+            for (int u = 0; u < KU; ++u) o[u] = 0.0;
+#pragma unroll
+            for (int l2 = 0; l2 < G / 2; ++l2) {
+#pragma unroll
+                for (int u = 0; u < KU; ++u) {
+                    const double2 gg = reinterpret_cast<const double2*>(Gr + (k0 + u) * G)[l2];
+                    if (EXACT || 2 * l2 < C) o[u] = dadd(o[u], dmul(gg.x, xr[2 * l2]));
+                    if (EXACT || 2 * l2 + 1 < C) o[u] = dadd(o[u], dmul(gg.y, xr[2 * l2 + 1]));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < KU; ++u)
+                if (EXACT || k0 + u < C) tr[k0 + u] = dmul(-4.0, dsub(tr[k0 + u], o[u]));
+        }
+        // y = x - tau * grad (solver.hpp:102)
+        bool fin = true;
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            if (EXACT || k < C) {
+                if constexpr (BT) ra[k] = tr[k];            // keep g_k for lin_i
+                const double y = dsub(xr[k], dmul(sp.tau, tr[k]));
+                fin = fin && isfinite(y);
+                tr[k] = y;
+            }
+        }
+        if (!fin) {
+            bad = true;
+        } else if (C == 1) {
+            tr[0] = 1.0;
+        } else {
+            const double thr = row_threshold<G>(tr, C);
+            double w[G];
+#pragma unroll
+            for (int k = 0; k < G; ++k) w[k] = (EXACT || k < C) ? ref_max(dsub(tr[k], thr), 0.0) : 0.0;
+            fold_residual<G>(w, C);
+#pragma unroll
+            for (int k = 0; k < G; ++k)
+                if (EXACT || k < C) tr[k] = w[k];
+        }
+        if constexpr (BT) {
+            double li = 0.0, qi = 0.0;
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                if (EXACT || k < C) {
+                    const double d = dsub(tr[k], xr[k]);
+                    li = dadd(li, dmul(ra[k], d));
+                    qi = dadd(qi, dmul(d, d));
+                }
+            }
+            b.rowterm[0][rb + lane] = li;
+            b.rowterm[1][rb + lane] = qi;
+            b.rowterm[2][rb + lane] = mi;
+        }
+    }
+    __syncwarp();
+    // 3: store bar^n
+#pragma unroll 4
+    for (int p = 0; p < 32; p += RPW) {
+        const unsigned long long r2 = rb + p + sub;
+        if (r2 < rend && lane_ok) sp.D[(size_t)(g.row0 + r2) * C + lg] = TX[(p + sub) * LD + lg];
+    }
+    __syncwarp();
+    return !bad;
+}
+
 template <int G, bool EXACT, bool BT = false>
 __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
     DevState* st = b.st;
     if (st->done) return;
     extern __shared__ double smt[];
     constexpr int LD = G + 1;
-    constexpr int RPW = 32 / G;
-    constexpr int KU = G < 4 ? G : 4;
     const int C = EXACT ? G : (int)g.C;
-    const unsigned lane = threadIdx.x & 31u;
-    const int lg = (int)(lane % G);
-    const int sub = (int)(lane / G);
     const int warp = threadIdx.x >> 5;
     double* Gr = smt;                                        // Gr[k*G + l] = G[k][l]
     double* TA = smt + G * G + warp * 3 * 32 * LD;
     double* TB = TA + 32 * LD;
     double* TX = TB + 32 * LD;
-    const int mode = st->step_mode;
-    const double* __restrict__ A = b.U[st->step_a];
-    const double* __restrict__ Bp = b.U[st->step_b];
-    double* __restrict__ D = b.U[st->step_dst];
-    const double beta = st->beta_step;
-    const double tau = st->tau;
-    const int sel = st->step_sel;
-    const double* __restrict__ XS = b.xs[st->xs_r * 2 + sel];
-    const double* __restrict__ Gt = b.gfull[sel];            // Gt[l*C + k] == G[k][l]
-    for (int e = threadIdx.x; e < G * G; e += blockDim.x) {
-        const int k = e / G, l = e % G;
-        Gr[e] = (k < C && l < C) ? Gt[l * C + k] : 0.0;
-    }
+    const StepPlan sp = step_plan(b);
+    stage_gram_matrix<G>(b, Gr, C);
     __syncthreads();
-
     const unsigned long long warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
-    const bool lane_ok = EXACT || lg < C;
-    double* ra = TA + lane * LD;                             // this thread's row in phase 2
-    const double* rb_ = TB + lane * LD;
-    double* tr = TX + lane * LD;
-    bool bad = false;
-    for (unsigned long long rb = w0 * 32; rb < g.nrows; rb += warps * 32) {
-        const bool row_ok = rb + lane < g.nrows;
-        // 1: async loads of the batch
-        for (int p = 0; p < 32; p += RPW) {
-            const unsigned long long row = rb + p + sub;
-            if (row < g.nrows && lane_ok) {
-                const size_t a = (size_t)(g.row0 + row) * C + lg;
-                const int t = (p + sub) * LD + lg;
-                cp_async8(TA + t, A + a);
-                if (mode != kLiteral) cp_async8(TB + t, Bp + a);
-                cp_async8(TX + t, XS + (size_t)row * C + lg);
-            }
-        }
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncwarp();
-        if (row_ok) {
-            double xr[G];
-#pragma unroll
-            for (int l = 0; l < G; ++l)
-                xr[l] = (EXACT || l < C) ? ((mode == kLiteral) ? ra[l] : extrap(ra[l], rb_[l], beta)) : 0.0;
-            double mi = 0.0;                                 // BT: <xs_i, x_i>, component order
-            if constexpr (BT) {
-#pragma unroll
-                for (int k = 0; k < G; ++k)
-                    if (EXACT || k < C) mi = dadd(mi, dmul(tr[k], xr[k]));
-            }
-            // gradient (objective.hpp:37-43, :116-117), KU independent chains
-#pragma unroll 1
-            for (int k0 = 0; k0 < C; k0 += KU) {
-                double o[KU];
-#pragma unroll
-                for (int u = 0; u < KU; ++u) o[u] = 0.0;
-#pragma unroll
-                for (int l2 = 0; l2 < G / 2; ++l2) {
-#pragma unroll
-                    for (int u = 0; u < KU; ++u) {
-                        const double2 gg = reinterpret_cast<const double2*>(Gr + (k0 + u) * G)[l2];
-                        if (EXACT || 2 * l2 < C) o[u] = dadd(o[u], dmul(gg.x, xr[2 * l2]));
-                        if (EXACT || 2 * l2 + 1 < C) o[u] = dadd(o[u], dmul(gg.y, xr[2 * l2 + 1]));
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < KU; ++u)
-                    if (EXACT || k0 + u < C) tr[k0 + u] = dmul(-4.0, dsub(tr[k0 + u], o[u]));
-            }
-            // y = x - tau * grad (solver.hpp:102)
-            bool fin = true;
-#pragma unroll
-            for (int k = 0; k < G; ++k) {
-                if (EXACT || k < C) {
-                    if constexpr (BT) ra[k] = tr[k];            // keep g_k for lin_i
-                    const double y = dsub(xr[k], dmul(tau, tr[k]));
-                    fin = fin && isfinite(y);
-                    tr[k] = y;
-                }
-            }
-            if (!fin) {
-                bad = true;
-            } else if (C == 1) {
-                tr[0] = 1.0;
-            } else {
-                const double thr = row_threshold<G>(tr, C);
-                double w[G];
-#pragma unroll
-                for (int k = 0; k < G; ++k) w[k] = (EXACT || k < C) ? ref_max(dsub(tr[k], thr), 0.0) : 0.0;
-                fold_residual<G>(w, C);
-#pragma unroll
-                for (int k = 0; k < G; ++k)
-                    if (EXACT || k < C) tr[k] = w[k];
-            }
-            if constexpr (BT) {
-                double li = 0.0, qi = 0.0;
-#pragma unroll
-                for (int k = 0; k < G; ++k) {
-                    if (EXACT || k < C) {
-                        const double d = dsub(tr[k], xr[k]);
-                        li = dadd(li, dmul(ra[k], d));
-                        qi = dadd(qi, dmul(d, d));
-                    }
-                }
-                b.rowterm[0][rb + lane] = li;
-                b.rowterm[1][rb + lane] = qi;
-                b.rowterm[2][rb + lane] = mi;
-            }
-        }
-        __syncwarp();
-        // 3: store bar^n
-#pragma unroll 4
-        for (int p = 0; p < 32; p += RPW) {
-            const unsigned long long r2 = rb + p + sub;
-            if (r2 < g.nrows && lane_ok) D[(size_t)(g.row0 + r2) * C + lg] = TX[(p + sub) * LD + lg];
-        }
-        __syncwarp();
+    bool ok = true;
+    for (unsigned long long rb = w0 * 32; rb < g.nrows; rb += warps * 32)
+        ok = step_t_batch<G, EXACT, BT>(sp, b, g, Gr, C, TA, TB, TX, rb, g.nrows) && ok;
+    if (!ok) {
+        st->error = 1;
+        st->done = 1;
     }
-    if (bad) {
+}
+
+// =============================================================================
+// K3 + K2 fused (C <= 32, FISTA without backtracking): the step kernel of
+// iteration n also accumulates the Gram partials of bar^n and of the next
+// extrapolated point X_ext^{n+1} = bar^n + beta_n (bar^n - bar^{n-1})
+// (solver.hpp:261), which it holds on chip anyway -- k_gram's separate pass
+// re-read both from HBM.  A CTA owns whole 1024-row blocks (grid-stride) and
+// walks each in 128-row chunks: every warp steps 32 rows (step_t_batch), the
+// extrapolated rows replace bar^{n-1} in the A tile, then the CTA's Gram
+// threads (one 4x4 tile of (r, s), r <= s, of one matrix each) add the chunk's
+// rows in ascending order -- the per-block sequential order of objective.hpp:71-80
+// is kept exactly, so the partials equal k_gram's bit for bit.
+// =============================================================================
+template <int G, bool EXACT>
+__global__ void __launch_bounds__(kStepThreads, 2) k_step_gram(Bufs b, Geo g) {
+    DevState* st = b.st;
+    if (st->done) return;
+    extern __shared__ double smt[];
+    constexpr int LD = G + 1;
+    constexpr int TS = G < 4 ? G : 4;
+    constexpr int NW = kStepThreads / 32;
+    const int C = EXACT ? G : (int)g.C;
+    const int warp = threadIdx.x >> 5;
+    double* Gr = smt;
+    double* TA0 = smt + G * G;                               // warp w: TA0 + w * 3 * 32 * LD
+    double* TA = TA0 + warp * 3 * 32 * LD;
+    double* TB = TA + 32 * LD;
+    double* TX = TB + 32 * LD;
+    const StepPlan sp = step_plan(b);
+    const double beta_n = st->beta_next;
+    // Gram tile of this thread: matrix 0 = bar^n (slot kMatBar), 1 = X_ext^{n+1} (kMatExt)
+    const int nT = (C + TS - 1) / TS;
+    const int tiles_per_mat = nT * (nT + 1) / 2;
+    const int tile = threadIdx.x;
+    const bool has = tile < 2 * tiles_per_mat;
+    const int mat = has ? tile / tiles_per_mat : 0;
+    int tt = has ? tile % tiles_per_mat : 0;
+    int I = 0;
+    while (tt >= nT - I) { tt -= nT - I; ++I; }
+    const int J = I + tt;
+    const int toff = mat == 0 ? 2 * 32 * LD : 0;             // bar^n in TX, ext in TA
+    // zero the padding columns once (never written; read by the Gram tiles)
+    if (!EXACT)
+        for (int e = threadIdx.x; e < NW * 3 * 32 * LD; e += blockDim.x)
+            if (e % LD >= C) TA0[e] = 0.0;
+    stage_gram_matrix<G>(b, Gr, C);
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31u;
+    bool ok = true;
+    for (unsigned long long blk = blockIdx.x; blk < g.nblk; blk += gridDim.x) {
+        const unsigned long long r0 = blk * kBlock;
+        const unsigned long long r1 = min(r0 + kBlock, g.nrows);
+        double acc[TS][TS];
+#pragma unroll
+        for (int a = 0; a < TS; ++a)
+#pragma unroll
+            for (int c = 0; c < TS; ++c) acc[a][c] = 0.0;
+        for (unsigned long long c0 = r0; c0 < r1; c0 += 32 * NW) {
+            const unsigned long long rb = c0 + 32 * warp;
+            if (rb < r1) {
+                ok = step_t_batch<G, EXACT, false>(sp, b, g, Gr, C, TA, TB, TX, rb, r1) && ok;
+                // X_ext^{n+1} rows in place of bar^{n-1} (lane = component)
+                constexpr int RPW = 32 / G;
+                const int lg = (int)(lane % G), sub = (int)(lane / G);
+                if (EXACT || lg < C)
+                    for (int p = 0; p < 32; p += RPW) {
+                        const int t = (p + sub) * LD + lg;
+                        TA[t] = extrap(TX[t], TA[t], beta_n);
+                    }
+            }
+            __syncthreads();
+            if (has) {
+                const int rows = (int)min((unsigned long long)(32 * NW), r1 - c0);
+                for (int q = 0; q < rows; ++q) {
+                    const double* row = TA0 + (q >> 5) * 3 * 32 * LD + toff + (q & 31) * LD;
+                    double xr[TS], xq[TS];
+#pragma unroll
+                    for (int a = 0; a < TS; ++a) {
+                        xr[a] = row[TS * I + a];
+                        xq[a] = row[TS * J + a];
+                    }
+#pragma unroll
+                    for (int a = 0; a < TS; ++a)
+#pragma unroll
+                        for (int c = 0; c < TS; ++c) acc[a][c] = dadd(acc[a][c], dmul(xr[a], xq[c]));
+                }
+            }
+            __syncthreads();
+        }
+        if (has) {
+            double* out = b.gpart[mat == 0 ? kMatBar : kMatExt] + blk * g.npairs;
+#pragma unroll
+            for (int a = 0; a < TS; ++a)
+#pragma unroll
+                for (int c = 0; c < TS; ++c) {
+                    const int r = TS * I + a, s = TS * J + c;
+                    if (r <= s && s < C) out[pair_index(r, s, C)] = acc[a][c];
+                }
+        }
+    }
+    if (!ok) {
         st->error = 1;
         st->done = 1;
     }

@@ -441,8 +441,8 @@ def test_upload_rejects_malformed_csr():
                          (np.array([0, 1, 0, 1, 2, 2], np.uint32), "not strictly ascending")):
             with pytest.raises(fc.InvalidInput, match=msg):
                 t.upload(SparseSimilarity(3, rp, col, None, 6.0))
-        with pytest.raises(fc.InvalidInput, match="row_ptr"):
-            t.upload(SparseSimilarity(3, np.array([0, 4, 2, 6], np.int64), good, None, 6.0))
+        with pytest.raises(fc.InvalidInput, match="row_ptr decreases at row 1"):
+            t.upload(SparseSimilarity(3, np.array([0, 1, 0, 6], np.int64), good, None, 6.0))
         g = SparseSimilarity(3, rp, good, None, 6.0)
         t.upload(g)
         x0 = np.full((3, 2), 0.5)
