@@ -74,6 +74,29 @@ def make_graph(cfg, threads=0, host_only=False):
                                 locality=cfg.get("locality", False), threads=threads)
 
 
+def shared_graph(cfg, name, rank, world):
+    """N > 1: rank 0 generates the graph once and writes it as an FCCSR001 file in
+    /dev/shm; every rank maps that file (zero-copy, one page-cache copy for the node)
+    instead of each rank regenerating the whole graph in host memory."""
+    import paper_2506_04045_b200 as fc
+    path = os.path.join("/dev/shm" if os.path.isdir("/dev/shm") else "/tmp",
+                        f"fc_bench_{name}_{cfg['n']}_{cfg['m']}_{GRAPH_SEED}.fccsr")
+    if rank == 0 and not os.path.exists(path):
+        g = make_graph(cfg)
+        tmp = path + f".{os.getpid()}.tmp"
+        fc.write_similarity_binary(g, tmp)
+        os.replace(tmp, path)
+        del g
+    barrier(world)
+    hdr = np.fromfile(path, dtype="<u8", count=5)
+    n, nnz = int(hdr[1]), int(hdr[2])
+    if int(hdr[3]) & 1:
+        raise RuntimeError("shared_graph: weighted bench graphs are not expected")
+    rp = np.memmap(path, dtype="<i8", mode="r", offset=40, shape=(n + 1,))
+    ci = np.memmap(path, dtype="<u4", mode="r", offset=40 + 8 * (n + 1), shape=(nnz,))
+    return fc.SparseSimilarity(n, rp, ci, None, float(nnz))
+
+
 def loss_hash(records, k):
     """SHA-256 of the float64 loss records of iterations 0..k (first record per iteration),
     little-endian bytes: identical bits <=> identical hash.  Both arms print it."""
@@ -300,7 +323,7 @@ def main():
 
     torch.cuda.set_device(local)
     t_setup = time.perf_counter()
-    graph = make_graph(cfg)
+    graph = make_graph(cfg) if world == 1 else shared_graph(cfg, args.config, rank, world)
     t_graph = time.perf_counter() - t_setup
     nccl_id = None
     if world > 1:

@@ -93,6 +93,16 @@ int fc_create(fc_ctx** out, int device, int rank, int world, const unsigned char
 /* Test topology: `shards` row shards emulated on ONE device (same kernels,
  * same partition and ordered cross-shard chain, no NCCL). */
 int fc_create_virtual(fc_ctx** out, int device, int shards);
+/* In-process loopback group (tests / single-GPU validation of the multi-rank path):
+ * `world` rank contexts in ONE process on `device`, one host thread per rank, each
+ * created with fc_create_loopback.  The collectives are stream-ordered device copies
+ * pulled from the peer after a CUDA event (no NCCL); the ranks run exactly the
+ * multi-rank code of fc_create(rank, world, nccl_id): shard partition, allgather,
+ * ordered recv -> combine -> send chain, broadcast from the last rank. */
+typedef struct fc_loopback fc_loopback;
+int fc_loopback_create(fc_loopback** out, int device, int world);
+void fc_loopback_destroy(fc_loopback* group);
+int fc_create_loopback(fc_ctx** out, fc_loopback* group, int rank);
 void fc_destroy(fc_ctx* ctx);
 
 /* SparseSimilarity (sparse.hpp:21-146).  Every rank passes the FULL CSR; the

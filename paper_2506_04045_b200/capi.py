@@ -61,6 +61,9 @@ SIGNATURES = {
     "fc_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "fc_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_char_p]),
     "fc_create_virtual": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int]),
+    "fc_loopback_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int]),
+    "fc_loopback_destroy": (None, [C.c_void_p]),
+    "fc_create_loopback": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int]),
     "fc_destroy": (None, [C.c_void_p]),
     "fc_upload_csr": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _i64p, _u32p, _dp, C.c_double]),
     "fc_partition": (C.c_int, [C.c_void_p, _u64p, C.c_int]),
@@ -182,14 +185,44 @@ def _take(ptr, count, dtype):
     return arr
 
 
+class LoopbackGroup:
+    """fc_loopback: `world` rank contexts of ONE process on one device (one host thread
+    per rank), exchanging through stream-ordered device copies instead of NCCL -- the
+    multi-rank code path (shards, allgather, ordered chain, broadcast) without 8 GPUs."""
+
+    def __init__(self, world: int, device: int = 0):
+        h = C.c_void_p()
+        rc = lib().fc_loopback_create(C.byref(h), device, world)
+        if rc:
+            raise_for(rc, lib().fc_last_error(None).decode())
+        self.h, self.world, self.device = h, world, device
+
+    def context(self, rank: int) -> "Context":
+        return Context(self.device, rank=rank, world=self.world, loopback=self)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fc_loopback_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
-    """One device (one process per GPU).  world > 1: NCCL row-sharded solver."""
+    """One device (one process per GPU).  world > 1: NCCL row-sharded solver
+    (or, with `loopback`, one rank of an in-process LoopbackGroup)."""
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 virtual_shards: int | None = None):
+                 virtual_shards: int | None = None, loopback: "LoopbackGroup | None" = None):
         L = lib()
         h = C.c_void_p()
-        if virtual_shards:
+        if loopback is not None:
+            rc = L.fc_create_loopback(C.byref(h), loopback.h, rank)
+        elif virtual_shards:
             rc = L.fc_create_virtual(C.byref(h), device, virtual_shards)
         else:
             rc = L.fc_create(C.byref(h), device, rank, world, nccl_id)

@@ -38,6 +38,7 @@
 
 #include "fc_internal.h"
 #include "fc_kernels.cuh"
+#include "fc_transport.h"
 #include "fuzzyclust_cuda.h"
 
 extern "C" int fc_generate_graph_impl(const fc_graph_spec* spec, uint64_t* nnz_out, int64_t** row_ptr_out,
@@ -97,7 +98,8 @@ struct fc_ctx {
     cudaStream_t side = nullptr;       // Gram next to the sweep (independent within an iteration)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool overlap = false;              // FC_OVERLAP=1: Gram on a side stream (measured: no gain)
-    ncclComm_t comm = nullptr;
+    int overlap2 = 0;                  // FC_OVERLAP=2[:k]: persistent Gram (k CTAs per SM) launched before the sweep
+    fc::Transport* xport = nullptr;    // multi-rank collectives (NCCL or in-process loopback); null = one rank
     int sm_count = 148;
     std::string err;
     std::atomic<uint64_t> launches{0};
@@ -147,13 +149,16 @@ struct fc_ctx {
     uint64_t enqueued = 0;             // iterations enqueued after begin
     uint64_t host_iter = 0;            // FISTA/GPA iteration index of the next enqueued pass
     uint64_t bt_max_host = 0;          // session's backtracking cap (pass budget of fc_solve)
+    int ag_buf = -1;                   // multi-rank backtracking: replica the next pass allgathers (device plan)
+    bool stop_seen = false;            // multi-rank backtracking: the device reported done
     unsigned long long csr_fp = 0;     // fingerprint of the resident shard CSR
     cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
 
     bool sweep_tma = false;            // FC_SWEEP=tma selects the TMA gather4 sweep
     bool sweep_groups = false;       // FC_SWEEP=groups: per-group row sweep for C <= 16
     bool step_big = false;             // FC_STEP=big: thread-per-row k_step_big for C > 32
-    bool fuse_gram = true;             // FC_FUSE=0: separate k_step_t + k_gram for C <= 32 FISTA
+    bool fuse_gram = false;            // FC_FUSE=1: fused k_step_gram for C <= 32 FISTA (measured slower: 8.5 vs 8.2 ms at C)
+    bool step_wide2 = true;            // FC_STEP=wide1: the round-1 k_step_wide (G streamed) for 32 < C <= 128
     bool umaps_ok = false;
     UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
 
@@ -207,6 +212,12 @@ int set_err(fc_ctx* ctx, int code, const char* fmt, ...) {
         if (r_ != ncclSuccess)                                                             \
             return set_err(ctx, FC_DEVICE, "NCCL error %s at %s:%d", ncclGetErrorString(r_), \
                            __FILE__, __LINE__);                                            \
+    } while (0)
+
+#define XP(call)                                              \
+    do {                                                      \
+        int rc_ = (call);                                     \
+        if (rc_) return set_err(ctx, rc_, "%s", ctx->err.c_str()); \
     } while (0)
 
 #define TRY(expr)                  \
@@ -418,6 +429,24 @@ int launch_step_gram(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     return FC_OK;
 }
 
+template <int CP>
+int launch_step_wide2(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
+    const size_t smem = Wide2Cfg<CP>::smem();
+    if (!grid) {
+        CU(cudaFuncSetAttribute(k_step_wide2<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_wide2<CP>, kW2Threads, smem, ctx->sm_count);
+    }
+    const unsigned long long need = (g.nrows + kW2Rows - 1) / kW2Rows;
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
+    k_step_wide2<CP><<<gr, kW2Threads, smem, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_wide2 launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
 template <int G, int S>
 struct LaunchStepGram {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g) {
@@ -470,7 +499,12 @@ struct LaunchStep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, int bt) {
         if (g.nrows == 0) return FC_OK;
         if constexpr (S > 1) {
-            if (!bt) return ctx->step_big ? launch_step_big<32 * S>(ctx, b, g) : launch_step_wide<32 * S>(ctx, b, g);
+            if (!bt) {
+                if (ctx->step_big) return launch_step_big<32 * S>(ctx, b, g);
+                if constexpr (S <= 4)
+                    if (ctx->step_wide2) return launch_step_wide2<32 * S>(ctx, b, g);
+                return launch_step_wide<32 * S>(ctx, b, g);
+            }
         }
         if (S == 1 && (!bt || G <= 16)) {   // thread-per-row projection (+ backtracking row terms;
             // at G = 32 those spill, the lane-parallel k_step below takes bt there)
@@ -677,7 +711,7 @@ Geo make_geo(fc_ctx* ctx, size_t s) {
 // final totals slot (what k_finalize reads)
 Bufs final_bufs(fc_ctx* ctx) {
     Bufs b = make_bufs(ctx, 0);
-    b.totals = ctx->d_totals + (ctx->comm ? 0 : (ctx->shards.size() - 1)) * nchains_of(ctx->c);
+    b.totals = ctx->d_totals + (ctx->xport ? 0 : (ctx->shards.size() - 1)) * nchains_of(ctx->c);
     return b;
 }
 
@@ -705,7 +739,7 @@ int phase_step_gram(fc_ctx* ctx) {
     return FC_OK;
 }
 
-int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr) {
+int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr, unsigned max_ctas = 0) {
     if (!strm) strm = ctx->stream;
     ProfScope p(ctx, kClsGram);
     const uint32_t c = ctx->c;
@@ -737,7 +771,8 @@ int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr) {
         if (g.nblk == 0) continue;
         const Bufs b = make_bufs(ctx, s);
         const int threads = std::min(kGramMaxThreads, (tiles + 31) / 32 * 32);
-        dim3 grid((unsigned)g.nblk, (unsigned)((tiles + threads - 1) / threads));
+        const unsigned gx = max_ctas ? (unsigned)std::min<unsigned long long>(g.nblk, max_ctas) : (unsigned)g.nblk;
+        dim3 grid(gx, (unsigned)((tiles + threads - 1) / threads));
         kfn<<<grid, threads, smem, strm>>>(b, g, dual ? 1 : 0, R);
         TRY(check_launch(ctx, "k_gram"));
     }
@@ -779,7 +814,7 @@ int phase_combine(fc_ctx* ctx, int mat_mask, int scal_mask) {
     const size_t nch = nchains_of(ctx->c);
     const int threads = kCombThreads;
     const int blocks = (int)((2 * npairs_of(ctx->c) + 31) / 32) + kNumScal;
-    if (!ctx->comm) {
+    if (!ctx->xport) {
         ProfScope p(ctx, kClsCombine);
         for (size_t s = 0; s < ctx->shards.size(); ++s) {
             const Bufs b = make_bufs(ctx, s);
@@ -792,7 +827,7 @@ int phase_combine(fc_ctx* ctx, int mat_mask, int scal_mask) {
     }
     if (ctx->rank > 0) {
         ProfScope p(ctx, kClsComm);
-        NC(ncclRecv(ctx->d_chain_in, nch, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+        XP(ctx->xport->recv_prev(ctx->d_chain_in, nch, ctx->stream, &ctx->err));
     }
     {
         ProfScope p(ctx, kClsCombine);
@@ -803,9 +838,8 @@ int phase_combine(fc_ctx* ctx, int mat_mask, int scal_mask) {
         TRY(check_launch(ctx, "k_combine"));
     }
     ProfScope p(ctx, kClsComm);
-    if (ctx->rank < ctx->world - 1)
-        NC(ncclSend(ctx->d_totals, nch, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
-    NC(ncclBroadcast(ctx->d_totals, ctx->d_totals, nch, ncclDouble, ctx->world - 1, ctx->comm, ctx->stream));
+    if (ctx->rank < ctx->world - 1) XP(ctx->xport->send_next(ctx->d_totals, nch, ctx->stream, &ctx->err));
+    XP(ctx->xport->bcast_last(ctx->d_totals, nch, ctx->stream, &ctx->err));
     return FC_OK;
 }
 
@@ -819,15 +853,9 @@ int phase_finalize(fc_ctx* ctx, int kind, int mat_mask) {
 
 // allgather of the rows of U[buf] each rank owns (NCCL contexts only)
 int phase_allgather(fc_ctx* ctx, int buf) {
-    if (!ctx->comm) return FC_OK;
+    if (!ctx->xport) return FC_OK;
     ProfScope p(ctx, kClsComm);
-    const uint32_t c = ctx->c;
-    NC(ncclGroupStart());
-    for (int r = 0; r < ctx->world; ++r) {
-        const size_t off = ctx->bounds[r] * c, cnt = (ctx->bounds[r + 1] - ctx->bounds[r]) * c;
-        NC(ncclBroadcast(ctx->d_U[buf] + off, ctx->d_U[buf] + off, cnt, ncclDouble, r, ctx->comm, ctx->stream));
-    }
-    NC(ncclGroupEnd());
+    XP(ctx->xport->allgather_rows(ctx->d_U[buf], ctx->bounds.data(), ctx->c, ctx->stream, &ctx->err));
     return FC_OK;
 }
 
@@ -845,7 +873,18 @@ int enqueue_prelude(fc_ctx* ctx) {   // FISTA loss at x0 (solver.hpp:206-212)
 // the heavy rows start at once.  Measured no gain (the persistent sweep holds the
 // register file until its tail), so the default is sequential.
 static int gram_and_sweep(fc_ctx* ctx) {
-    if (ctx->overlap && !ctx->comm && !ctx->profiling) {
+    if (ctx->overlap2 && !ctx->profiling) {
+        // persistent Gram grid (one CTA per SM) launched FIRST on the side stream, then the
+        // sweep: the FP64-bound Gram runs in the memory stalls of the HBM-bound sweep
+        CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
+        CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+        TRY(phase_gram(ctx, true, ctx->side, (unsigned)ctx->sm_count * ctx->overlap2));
+        TRY(phase_sweep(ctx, true));
+        CU(cudaEventRecord(ctx->join_ev, ctx->side));
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+        return FC_OK;
+    }
+    if (ctx->overlap && !ctx->xport && !ctx->profiling) {
         CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
         CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
         TRY(phase_sweep(ctx, true));
@@ -865,7 +904,7 @@ int enqueue_fista_iteration(fc_ctx* ctx, int bt) {
         TRY(phase_sweep(ctx, true));
     } else {
         TRY(phase_step(ctx, bt));
-        TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
+        TRY(phase_allgather(ctx, ctx->ag_buf >= 0 ? ctx->ag_buf : (int)(ctx->host_iter % 3)));
         TRY(gram_and_sweep(ctx));
     }
     TRY(phase_rowsum(ctx, bt));
@@ -1091,7 +1130,7 @@ int ensure_trace(fc_ctx* ctx, uint64_t records) {
     return FC_OK;
 }
 
-bool granular_ok(fc_ctx* ctx) { return ctx->comm == nullptr; }
+bool granular_ok(fc_ctx* ctx) { return ctx->xport == nullptr; }
 
 }  // namespace
 
@@ -1105,7 +1144,7 @@ static int upload_csr_impl(fc_ctx*, uint64_t, uint64_t, const int64_t*, const ui
 int fc_internal_h2d(fc_ctx* ctx, void* dst, const void* src, size_t bytes) { return h2d_big(ctx, dst, src, bytes); }
 int fc_internal_csr(fc_ctx* ctx, uint64_t* n, const long long** row_ptr, const unsigned** col, const double** val) {
     if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
-    if (ctx->comm) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
+    if (ctx->xport) return set_err(ctx, FC_INVALID, "granular operators need a single-rank context");
     *n = ctx->n;
     *row_ptr = ctx->d_row_ptr;
     *col = ctx->d_col;
@@ -1135,7 +1174,8 @@ int fc_nccl_unique_id(unsigned char id[128]) {
     return FC_OK;
 }
 
-static int create_common(fc_ctx** out, int device, int rank, int world, int vshards, const unsigned char* id) {
+static int create_common(fc_ctx** out, int device, int rank, int world, int vshards, const unsigned char* id,
+                         fc_loopback* loop = nullptr) {
     fc_ctx* ctx = nullptr;
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) return set_err(nullptr, FC_INVALID, "bad rank/world");
@@ -1162,8 +1202,11 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         ctx->sweep_tma = std::strcmp(sw, "tma") == 0;
         ctx->sweep_groups = std::strcmp(sw, "groups") == 0;
     }
-    if (const char* sp = std::getenv("FC_STEP")) ctx->step_big = std::strcmp(sp, "big") == 0;
-    if (const char* fu = std::getenv("FC_FUSE")) ctx->fuse_gram = std::strcmp(fu, "0") != 0;
+    if (const char* sp = std::getenv("FC_STEP")) {
+        ctx->step_big = std::strcmp(sp, "big") == 0;
+        ctx->step_wide2 = std::strcmp(sp, "wide1") != 0;
+    }
+    if (const char* fu = std::getenv("FC_FUSE")) ctx->fuse_gram = std::strcmp(fu, "1") == 0;
     if (const char* gr = std::getenv("FC_GRAPHS")) ctx->graphs = std::strcmp(gr, "0") != 0;
     {
         const unsigned hw = std::thread::hardware_concurrency();
@@ -1174,7 +1217,10 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
     CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
-    if (const char* ov = std::getenv("FC_OVERLAP")) ctx->overlap = std::strcmp(ov, "1") == 0;
+    if (const char* ov = std::getenv("FC_OVERLAP")) {
+        ctx->overlap = std::strcmp(ov, "1") == 0;
+        if (ov[0] == '2') ctx->overlap2 = ov[1] == ':' ? std::max(1, std::atoi(ov + 2)) : 1;
+    }
     CU(cudaMalloc(&ctx->d_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_done, 2 * sizeof(int)));
@@ -1185,10 +1231,14 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
     // FC_FORCE_NCCL=1 with world == 1 and an id: a 1-rank communicator, so the
     // NCCL allgather / ordered-chain code runs on a single GPU (test hook).
     const char* force = std::getenv("FC_FORCE_NCCL");
-    if (world > 1 || (id && force && *force == '1')) {
+    if (loop) {
+        ctx->xport = new fc::LoopbackTransport(loop, rank);
+    } else if (world > 1 || (id && force && *force == '1')) {
         ncclUniqueId u;
         std::memcpy(u.internal, id, 128);
-        NC(ncclCommInitRank(&ctx->comm, world, u, rank));
+        ncclComm_t comm = nullptr;
+        NC(ncclCommInitRank(&comm, world, u, rank));
+        ctx->xport = new fc::NcclTransport(comm, rank, world);
     }
     TRY(ensure_trace(ctx, 1024));
     CU(cudaFuncSetAttribute(k_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCombSmem));
@@ -1198,6 +1248,45 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
 int fc_create(fc_ctx** out, int device, int rank, int world, const unsigned char* nccl_id) {
     if (world > 1 && !nccl_id) return set_err(nullptr, FC_INVALID, "world > 1 needs an NCCL unique id");
     int rc = create_common(out, device, rank, world, 1, nccl_id);
+    if (rc && *out) {
+        g_thread_err = (*out)->err;
+        fc_destroy(*out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+int fc_loopback_create(fc_loopback** out, int device, int world) {
+    fc_ctx* ctx = nullptr;
+    *out = nullptr;
+    if (world < 1 || world > 64) return set_err(nullptr, FC_INVALID, "loopback: world must be in [1, 64]");
+    CU(cudaSetDevice(device));
+    auto* g = new fc_loopback();
+    g->world = world;
+    g->device = device;
+    g->slots.resize((size_t)fc_loopback::kKinds * world * fc_loopback::kRing);
+    for (auto& sl : g->slots) {
+        if (cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming) != cudaSuccess) {
+            fc_loopback_destroy(g);
+            return set_err(nullptr, FC_DEVICE, "loopback: cudaEventCreate failed");
+        }
+    }
+    if (const char* t = std::getenv("FC_LOOPBACK_TIMEOUT_S")) g->timeout_s = std::max(1.0, std::atof(t));
+    *out = g;
+    return FC_OK;
+}
+
+void fc_loopback_destroy(fc_loopback* g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    for (auto& sl : g->slots)
+        if (sl.ev) cudaEventDestroy(sl.ev);
+    delete g;
+}
+
+int fc_create_loopback(fc_ctx** out, fc_loopback* group, int rank) {
+    if (!group) return set_err(nullptr, FC_INVALID, "loopback: null group");
+    int rc = create_common(out, group->device, rank, group->world, 1, nullptr, group);
     if (rc && *out) {
         g_thread_err = (*out)->err;
         fc_destroy(*out);
@@ -1224,7 +1313,7 @@ void fc_destroy(fc_ctx* ctx) {
     prof_harvest(ctx);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->iter_exec) cudaGraphExecDestroy(ctx->iter_exec);
-    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    delete ctx->xport;
     for (int k = 0; k < 3; ++k) dfree(ctx, &ctx->d_U[k]);
     for (int k = 0; k < 4; ++k) dfree(ctx, &ctx->d_xs[k]);
     for (int k = 0; k < 3; ++k) dfree(ctx, &ctx->d_rowterm[k]);
@@ -1680,8 +1769,6 @@ int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const 
     if (cfg->method < FC_GPA || cfg->method > FC_FISTA_BT) return set_err(ctx, FC_INVALID, "solver: unknown method");
     const bool bt = cfg->method == FC_FISTA_BT;
     if (bt && !(cfg->bt_eta > 1.0)) return set_err(ctx, FC_INVALID, "solver: backtracking eta must be > 1");
-    if (bt && ctx->comm)
-        return set_err(ctx, FC_INVALID, "solver: backtracking FISTA needs a single-rank context");
     if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
     if (c == 0) return set_err(ctx, FC_INVALID, "membership: empty matrix");
     {
@@ -1730,6 +1817,8 @@ int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const 
     ctx->enqueued = 0;
     ctx->host_iter = cfg->method == FC_GPA ? 0 : 1;
     ctx->bt_max_host = cfg->bt_max;
+    ctx->stop_seen = false;
+    ctx->ag_buf = -1;
     ctx->session = true;
     if (cfg->method != FC_GPA) TRY(enqueue_prelude(ctx));
     return FC_OK;
@@ -1761,7 +1850,7 @@ static std::vector<char> iteration_key(fc_ctx* ctx) {
 // iteration of a session enqueues the same kernels with the same arguments):
 // removes the per-kernel launch gaps that dominate small-N iterations.
 static int launch_iteration(fc_ctx* ctx) {
-    if (!ctx->graphs || ctx->comm || ctx->profiling) return enqueue_iteration(ctx);
+    if (!ctx->graphs || ctx->xport || ctx->profiling) return enqueue_iteration(ctx);
     std::vector<char> key = iteration_key(ctx);
     if (!ctx->iter_exec || key != ctx->iter_key) {
         if (ctx->iter_exec) {
@@ -1795,6 +1884,25 @@ static int launch_iteration(fc_ctx* ctx) {
 int fc_solver_run(fc_ctx* ctx, uint64_t iterations) {
     if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
     CU(cudaSetDevice(ctx->device));
+    if (ctx->xport && ctx->method == FC_FISTA_BT) {
+        // A rejected line-search trial repeats its iteration into the same replica, so
+        // which replica a pass writes (and every rank must allgather) is a device
+        // decision: read the plan before each pass.  All ranks hold identical state, so
+        // they take the same number of passes and make the same collective calls.
+        for (uint64_t k = 0; k < iterations; ++k) {
+            TRY(download_state(ctx));
+            if (ctx->h_state->done || ctx->h_state->error) {
+                ctx->stop_seen = true;
+                break;
+            }
+            ctx->ag_buf = ctx->h_state->step_dst;
+            const int rc = launch_iteration(ctx);
+            ctx->ag_buf = -1;
+            TRY(rc);
+            ctx->enqueued++;
+        }
+        return FC_OK;
+    }
     for (uint64_t k = 0; k < iterations; ++k) {
         TRY(launch_iteration(ctx));
         ctx->enqueued++;
@@ -1866,7 +1974,7 @@ static int run_to_end(fc_ctx* ctx) {
     const uint64_t chunk = 8;
     uint64_t chunks = 0;
     int pending = -1;
-    while (ctx->enqueued < limit) {
+    while (ctx->enqueued < limit && !ctx->stop_seen) {
         const uint64_t k = std::min(chunk, limit - ctx->enqueued);
         TRY(fc_solver_run(ctx, k));
         const int slot = (int)(chunks++ & 1);
@@ -1960,7 +2068,7 @@ extern "C" {
 
 int fc_solver_checkpoint(fc_ctx* ctx, const char* path) {
     if (!ctx || !ctx->session) return set_err(ctx, FC_INVALID, "no solver session (call fc_solver_begin)");
-    if (ctx->comm) return set_err(ctx, FC_INVALID, "checkpoint: needs a single-rank context");
+    if (ctx->xport) return set_err(ctx, FC_INVALID, "checkpoint: needs a single-rank context");
     CU(cudaSetDevice(ctx->device));
     int done = 0;
     TRY(session_done(ctx, &done));                          // all enqueued passes finished
@@ -2007,7 +2115,7 @@ int fc_solver_checkpoint(fc_ctx* ctx, const char* path) {
 
 int fc_solver_resume(fc_ctx* ctx, const char* path) {
     if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
-    if (ctx->comm) return set_err(ctx, FC_INVALID, "checkpoint: needs a single-rank context");
+    if (ctx->xport) return set_err(ctx, FC_INVALID, "checkpoint: needs a single-rank context");
     CU(cudaSetDevice(ctx->device));
     FILE* f = std::fopen(path, "rb");
     if (!f) return ckpt_io_err(ctx, "open", path);

@@ -998,7 +998,8 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
     const double* __restrict__ Bm = b.U[st->sw_b];
     const double* __restrict__ Pm = dual ? b.U[st->sw_p] : nullptr;
     const double beta = st->beta_next;
-    const unsigned long long blk = blockIdx.x;
+    // grid-stride over blocks (a persistent grid can run next to the sweep, FC_OVERLAP=2)
+    for (unsigned long long blk = blockIdx.x; blk < g.nblk; blk += gridDim.x) {
     const unsigned long long r0 = blk * kBlock;
     const unsigned long long r1 = min(r0 + kBlock, g.nrows);
     const int R = rows_per_chunk;
@@ -1089,6 +1090,8 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
                 const int r = TS * I + a, s = TS * J + c;
                 if (r <= s && s < C) out[pair_index(r, s, C)] = acc[a][c];
             }
+    }
+    __syncthreads();                                         // stages are re-filled by the next block
     }
 }
 
@@ -1743,6 +1746,10 @@ __device__ __forceinline__ void fold_residual(double (&w)[CP], int C) {
 // G (power of two, 2..32) is the padded row width, C <= G; EXACT: C == G.
 constexpr int kStepThreads = 128;
 
+#ifndef FC_STEP_KU
+#define FC_STEP_KU 4
+#endif
+
 // Per-kernel invariants of a k_step_t / k_step_gram batch (read from the plan once).
 struct StepPlan {
     const double* A;                                         // bar^{n-1} (or the literal point)
@@ -1787,7 +1794,7 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
                                              unsigned long long rend) {
     constexpr int LD = G + 1;
     constexpr int RPW = 32 / G;
-    constexpr int KU = G < 4 ? G : 4;
+    constexpr int KU = G < FC_STEP_KU ? G : FC_STEP_KU;   // independent gradient chains per thread
     const unsigned lane = threadIdx.x & 31u;
     const int lg = (int)(lane % G);
     const int sub = (int)(lane / G);
@@ -2437,6 +2444,238 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
             if (k < C) D[(size_t)(g.row0 + rb + r) * C + k] = TY[r * LD + k];
         }
         __syncthreads();
+    }
+    if (bad) {
+        st->error = 1;
+        st->done = 1;
+    }
+}
+
+// =============================================================================
+// K3 for 32 < C <= 128 (no backtracking terms), v2: G resident in shared memory
+// for the whole launch, batches of 32 rows per CTA of 256 threads:
+//   1 X_ext rows -> TX (formed in registers, solver.hpp:261), S X_ext -> TY (cp.async)
+//   2 gradient as a register-tiled GEMM: thread (row group of 4 = its warp, k group
+//     of KT = CP/32 adjacent components) accumulates o[r][k] = sum_{l ascending}
+//     G[k][l] x_r[l] -- each output one sequential DMUL+DADD chain, the reference's
+//     order (objective.hpp:37-43); no barrier inside the l loop
+//   3 y = x - tau (-4 (xs - o)) in place of xs (objective.hpp:116-117, solver.hpp:102)
+//   4 projection (simplex.hpp:18-59): 8 lanes per row hold VPL = CP/8 values each and
+//     run a register bitonic network (in-lane stages, cross-lane stages by shuffle);
+//     the sorted row goes to TX, where one thread per row does the sequential cumsum /
+//     threshold and the residual folds (sequential sums in index order)
+//   5 coalesced store of bar^n.
+// Padding: G is zero outside C x C and x is zero beyond C, so the padded GEMM terms
+// add +0 to chains that start at +0 and can never be -0: exact.
+// =============================================================================
+constexpr int kW2Threads = 256;
+constexpr int kW2Rows = 32;
+
+template <int CP>
+struct Wide2Cfg {
+    static constexpr int LD = CP + 1;
+    static constexpr int KT = CP / 32;                      // k per thread in the GEMM
+    static constexpr int VPL = CP / 8;                      // values per lane in the projection
+    static size_t smem() { return sizeof(double) * ((size_t)CP * CP + (size_t)2 * kW2Rows * LD); }
+};
+
+template <int CP>
+__global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
+    DevState* st = b.st;
+    if (st->done) return;
+    constexpr int LD = Wide2Cfg<CP>::LD;
+    constexpr int KT = Wide2Cfg<CP>::KT;
+    constexpr int VPL = Wide2Cfg<CP>::VPL;
+    constexpr int R = kW2Rows;
+    extern __shared__ double smw2[];
+    double* GS = smw2;                                       // GS[l*CP + k] = G[k][l]
+    double* TX = GS + CP * CP;
+    double* TY = TX + R * LD;
+    __shared__ double thr_s[R];
+    __shared__ int work_s[R];
+    const int C = (int)g.C;
+    const int tid = threadIdx.x;
+    const StepPlan sp = step_plan(b);
+    {
+        const double* __restrict__ Gt = b.gfull[st->step_sel];   // Gt[l*C + k] == G[k][l]
+        for (int e = tid; e < CP * CP; e += kW2Threads) {
+            const int l = e / CP, k = e % CP;
+            GS[e] = (l < C && k < C) ? Gt[l * C + k] : 0.0;
+        }
+    }
+    const int rg = tid >> 5, kg = tid & 31;                  // GEMM: rows 4rg..4rg+3, k = KT*kg + j
+    const int pr = tid >> 3, pq = tid & 7;                   // projection: row pr, lane pq of 8
+    const unsigned gmask = 0xFFu << ((tid & 31) & ~7);
+    bool bad = false;
+    for (unsigned long long rb = (unsigned long long)blockIdx.x * R; rb < g.nrows;
+         rb += (unsigned long long)gridDim.x * R) {
+        const int rows = (int)min((unsigned long long)R, g.nrows - rb);
+        __syncthreads();                                     // previous batch's tiles consumed (and GS staged)
+        // 1: X_ext rows (registers -> TX), S X_ext rows -> TY
+        for (int e = tid; e < R * CP; e += kW2Threads) {
+            const int r = e / CP, k = e % CP;
+            double xv = 0.0;
+            if (r < rows && k < C) {
+                const size_t a = (size_t)(g.row0 + rb + r) * C + k;
+                const double av = ldg(sp.A + a);
+                xv = (sp.mode == kLiteral) ? av : extrap(av, ldg(sp.Bp + a), sp.beta);
+                cp_async8(TY + r * LD + k, sp.XS + (size_t)(rb + r) * C + k);
+            }
+            TX[r * LD + k] = xv;
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        // 2: GEMM
+        double o[4][KT];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < KT; ++j) o[i][j] = 0.0;
+        {
+            const double* xrow = TX + (4 * rg) * LD;
+            const double* gcol = GS + KT * kg;
+#pragma unroll 4
+            for (int l = 0; l < CP; ++l) {
+                double xv[4], gv[KT];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) xv[i] = xrow[i * LD + l];
+                if constexpr (KT % 2 == 0) {
+#pragma unroll
+                    for (int j = 0; j < KT; j += 2) {
+                        const double2 t = *reinterpret_cast<const double2*>(gcol + l * CP + j);
+                        gv[j] = t.x;
+                        gv[j + 1] = t.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < KT; ++j) gv[j] = gcol[l * CP + j];
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < KT; ++j) o[i][j] = dadd(o[i][j], dmul(gv[j], xv[i]));
+            }
+        }
+        // 3: grad and step, in place of xs
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = 4 * rg + i;
+#pragma unroll
+            for (int j = 0; j < KT; ++j) {
+                const int k = KT * kg + j;
+                if (r < rows && k < C) {
+                    const double grad = dmul(-4.0, dsub(TY[r * LD + k], o[i][j]));
+                    TY[r * LD + k] = dsub(TX[r * LD + k], dmul(sp.tau, grad));
+                }
+            }
+        }
+        __syncthreads();
+        // 4a: 8 lanes per row: finiteness, register bitonic sort (descending) -> TX
+        const bool live = pr < rows;
+        double v[VPL];
+        bool fin = true;
+#pragma unroll
+        for (int m = 0; m < VPL; ++m) {
+            const int k = VPL * pq + m;
+            const double y = (live && k < C) ? TY[pr * LD + k] : -INFINITY;
+            if (live && k < C && !isfinite(y)) fin = false;
+            v[m] = y;
+        }
+        const bool row_fin = __all_sync(gmask, fin);
+        if (live && !row_fin) bad = true;
+        const bool work = live && row_fin && C > 1;
+#pragma unroll
+        for (int kk = 2; kk <= CP; kk <<= 1) {
+#pragma unroll
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                if (j >= VPL) {                              // partner in lane pq ^ (j / VPL), same slot
+                    const int i0 = VPL * pq;
+                    const bool lower = (i0 & j) == 0;
+                    const bool keep_max = lower == ((i0 & kk) == 0);
+#pragma unroll
+                    for (int m = 0; m < VPL; ++m) {
+                        const double p = __shfl_xor_sync(gmask, v[m], j / VPL);
+                        const double mx = (v[m] < p) ? p : v[m];
+                        const double mn = (v[m] < p) ? v[m] : p;
+                        v[m] = keep_max ? mx : mn;
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < VPL; ++m) {
+                        const int l = m ^ j;
+                        if (l > m) {
+                            const int i = VPL * pq + m;
+                            const double a = v[m], c2 = v[l];
+                            const bool sw = ((i & kk) == 0) ? (a < c2) : (c2 < a);
+                            v[m] = sw ? c2 : a;
+                            v[l] = sw ? a : c2;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < VPL; ++m) TX[pr * LD + VPL * pq + m] = v[m];
+        if (pq == 0) work_s[pr] = work ? 1 : 0;
+        __syncthreads();
+        // 4b: one thread per row: sequential cumsum / threshold (simplex.hpp:29-36)
+        if (tid < R) {
+            const int r = tid;
+            double thr = 0.0;
+            if (work_s[r]) {
+                const double* sr = TX + r * LD;
+                double cs = 0.0, a_star = 0.0;
+                int k_star = -1;
+                for (int k = 0; k < C; ++k) {
+                    const double sk = sr[k];
+                    cs = dadd(cs, sk);
+                    const double a = dsub(cs, 1.0);
+                    if (threshold_cond(sk, a, (double)(k + 1))) {
+                        k_star = k;
+                        a_star = a;
+                    }
+                }
+                thr = k_star >= 0 ? a_star / (double)(k_star + 1) : 0.0;
+            }
+            thr_s[r] = thr;
+        }
+        __syncthreads();
+        // 4c: clip (every lane its slots)
+        if (work) {
+            const double thr = thr_s[pr];
+#pragma unroll
+            for (int m = 0; m < VPL; ++m) {
+                const int k = VPL * pq + m;
+                if (k < C) TY[pr * LD + k] = ref_max(dsub(TY[pr * LD + k], thr), 0.0);
+            }
+        } else if (live && row_fin && C == 1 && pq == 0) {
+            TY[pr * LD] = 1.0;
+        }
+        __syncthreads();
+        // 4d: residual folds (simplex.hpp:43-55), one thread per row, index order
+        if (tid < R && work_s[tid]) {
+            double* ty = TY + tid * LD;
+            for (int round = 0; round < 4; ++round) {
+                double sum = 0.0;
+                for (int k = 0; k < C; ++k) sum = dadd(sum, ty[k]);
+                const double residual = dsub(sum, 1.0);
+                if (residual == 0.0) break;
+                double top = ty[0];
+                for (int k = 1; k < C; ++k) top = (top < ty[k]) ? ty[k] : top;
+                int ties = 0;
+                for (int k = 0; k < C; ++k) ties += (ty[k] == top);
+                const double share = residual / (double)ties;
+                for (int k = 0; k < C; ++k)
+                    if (ty[k] == top) ty[k] = ref_max(dsub(ty[k], share), 0.0);
+            }
+        }
+        __syncthreads();
+        // 5: store bar^n
+        for (int e = tid; e < rows * CP; e += kW2Threads) {
+            const int r = e / CP, k = e % CP;
+            if (k < C) sp.D[(size_t)(g.row0 + rb + r) * C + k] = TY[r * LD + k];
+        }
     }
     if (bad) {
         st->error = 1;
