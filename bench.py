@@ -309,6 +309,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--parity-mode", type=int, default=0, choices=[0, 1],
+                    help="numerical contract of the timed solve: 0 bitwise (default), 1 tolerance mode")
+    ap.add_argument("--no-tolerance-leg", action="store_true",
+                    help="skip the extra tolerance-mode timing reported under 'tolerance_mode'")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -332,6 +336,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     ctx = capi.Context(local, rank=rank, world=world, nccl_id=nccl_id)
+    ctx.set_parity_mode(args.parity_mode)
     x0 = fc.init_membership(cfg["n"], cfg["c"], fc.InitStrategy(fc.InitKind.kRandom, X0_SEED), ctx=ctx)
     ctx.upload(graph)
     bounds = ctx.partition()
@@ -382,6 +387,40 @@ def main():
         valid_count = iters_done >= total
         prof_iters = max(0, min(args.steps, iters_done - total))
     value = args.steps / (ms / 1e3)
+
+    # ---- tolerance mode (fc_set_parity_mode 1), reported beside the bitwise headline ------
+    tol_leg = None
+    if args.parity_mode == 0 and not args.no_tolerance_leg and cfg["c"] <= 128 and method != capi.FISTA_BT:
+        ctx.set_parity_mode(1)
+        ctx.begin(x0, capi.Context.config(method=method, max_iter=args.warmup + 2 * args.steps + 1,
+                                          fista_restart=True))
+        ctx.run(args.warmup)
+        ctx.sync()
+        barrier(world)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.run(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        tms = allmax(e0.elapsed_time(e1), world)
+        ctx.set_profiling(True)
+        ctx.run(args.steps)
+        ctx.sync()
+        tkt = ctx.kernel_times()
+        ctx.set_profiling(False)
+        tdone = ctx.sync()
+        tres = ctx.end(graph.n, cfg["c"], want_x=False)
+        ctx.set_parity_mode(0)
+        it_b_tol = 8 * (graph.n + 1) + 12 * graph.nnz + 8 * cfg["c"] * graph.nnz + 6 * 8 * cfg["c"] * graph.n
+        tol_leg = {"value": args.steps / (tms / 1e3), "unit": "iter/s", "ms_per_step": tms / args.steps,
+                   "valid": bool(not tdone or tres["iterations"] >= args.warmup + 2 * args.steps),
+                   "kernel_ms_per_step": {k: v[0] / args.steps for k, v in tkt.items()},
+                   "iteration_bytes": it_b_tol,
+                   "achieved_gbs": it_b_tol * args.steps / (tms / 1e3) / 1e9,
+                   "contract": "north star: loss 1e-9 rel per record, U 1e-7, identical supports "
+                               "(single-gather FISTA by linearity + FMA contractions)"}
 
     # ---- end to end through the public call (host buffers) -------------------------------
     e2e = None
@@ -483,6 +522,18 @@ def main():
                                                                 rr["membership"].view(np.uint64))),
                 "supports_equal": bool(np.array_equal(gr["membership"] == 0, rr["membership"] == 0)),
             }
+            if tol_leg is not None:                    # the tolerance mode against the same reference run
+                ctx.set_parity_mode(1)
+                tr = ctx.solve(x0, capi.Context.config(method=plain, max_iter=rr["iters"], fista_restart=True),
+                               want_x=True)
+                ctx.set_parity_mode(0)
+                want = {it: loss for it, loss in rr["records"]}
+                rel = max(abs(loss - want[it]) / abs(want[it]) for it, loss, *_ in tr["records"])
+                tol_leg["vs_reference"] = {
+                    "iterations": rr["iters"], "max_rel_loss_diff": rel,
+                    "membership_max_abs_diff": float(np.abs(tr["membership"] - rr["membership"]).max()),
+                    "supports_equal": bool(np.array_equal(tr["membership"] == 0, rr["membership"] == 0)),
+                    "iterations_equal": int(tr["iterations"]) == rr["iters"]}
             if rr.get("sim") is not None:
                 del rr["sim"]
 
@@ -510,6 +561,8 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "parity": parity,
+            "parity_mode": args.parity_mode,
+            "tolerance_mode": tol_leg,
             "clocks": clk.summary(),
             "valid": bool(valid_count),
         }

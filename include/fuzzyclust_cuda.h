@@ -93,6 +93,17 @@ int fc_create(fc_ctx** out, int device, int rank, int world, const unsigned char
 /* Test topology: `shards` row shards emulated on ONE device (same kernels,
  * same partition and ordered cross-shard chain, no NCCL). */
 int fc_create_virtual(fc_ctx** out, int device, int shards);
+/* Numerical contract of the solver entry points (fc_solve / fc_solver_*):
+ *   0 (default) bitwise: the reference's operation order, no FMA -- results equal the
+ *     reference CPU solver bit for bit;
+ *   1 tolerance (north star: loss within 1e-9 relative at every record, U within 1e-7,
+ *     identical supports): FISTA gathers one operand per sweep (S X_ext^{n+1} formed by
+ *     linearity from S bar^n and S bar^{n-1}, solver.hpp:261 applied to S x) and the
+ *     Gram / gradient contractions use fused multiply-add.  GPA and FISTA without
+ *     backtracking, C <= 128.  Granular operators stay bitwise. */
+int fc_set_parity_mode(fc_ctx* ctx, int mode);
+int fc_get_parity_mode(const fc_ctx* ctx);
+
 /* In-process loopback group (tests / single-GPU validation of the multi-rank path):
  * `world` rank contexts in ONE process on `device`, one host thread per rank, each
  * created with fc_create_loopback.  The collectives are stream-ordered device copies

@@ -61,6 +61,8 @@ SIGNATURES = {
     "fc_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "fc_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_char_p]),
     "fc_create_virtual": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int]),
+    "fc_set_parity_mode": (C.c_int, [C.c_void_p, C.c_int]),
+    "fc_get_parity_mode": (C.c_int, [C.c_void_p]),
     "fc_loopback_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int]),
     "fc_loopback_destroy": (None, [C.c_void_p]),
     "fc_create_loopback": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int]),
@@ -231,6 +233,13 @@ class Context:
         self.h = h
         self.device, self.rank, self.world = device, rank, world
         self.n = None
+
+    def set_parity_mode(self, mode: int) -> None:
+        """0 = bitwise (default), 1 = tolerance mode (see include/fuzzyclust_cuda.h)."""
+        self._c(lib().fc_set_parity_mode(self.h, int(mode)))
+
+    def parity_mode(self) -> int:
+        return int(lib().fc_get_parity_mode(self.h))
 
     def close(self):
         if getattr(self, "h", None):

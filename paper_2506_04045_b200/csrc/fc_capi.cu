@@ -158,6 +158,7 @@ struct fc_ctx {
     bool sweep_groups = false;       // FC_SWEEP=groups: per-group row sweep for C <= 16
     bool step_big = false;             // FC_STEP=big: thread-per-row k_step_big for C > 32
     bool fuse_gram = false;            // FC_FUSE=1: fused k_step_gram for C <= 32 FISTA (measured slower: 8.5 vs 8.2 ms at C)
+    bool tol = false;                  // fc_set_parity_mode(1): tolerance mode (FMA, single-gather FISTA)
     bool step_wide2 = true;            // FC_STEP=wide1: the round-1 k_step_wide (G streamed) for 32 < C <= 128
     bool umaps_ok = false;
     UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
@@ -394,18 +395,18 @@ struct LaunchSweep {
     }
 };
 
-template <int G, bool EXACT, bool BT>
+template <int G, bool EXACT, bool BT, bool TOL = false>
 int launch_step_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     static PerDevice<int> grid_pd;
     int& grid = grid_pd(ctx);
     const size_t smem = step_t_smem(G);
     if (!grid) {
-        CU(cudaFuncSetAttribute(k_step_t<G, EXACT, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        grid = grid_for((const void*)k_step_t<G, EXACT, BT>, kStepThreads, smem, ctx->sm_count);
+        CU(cudaFuncSetAttribute(k_step_t<G, EXACT, BT, TOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_t<G, EXACT, BT, TOL>, kStepThreads, smem, ctx->sm_count);
     }
     const unsigned long long need = (g.nrows + 32 * (kStepThreads / 32) - 1) / (32 * (kStepThreads / 32));
     const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
-    k_step_t<G, EXACT, BT><<<gr, kStepThreads, smem, ctx->stream>>>(b, g);
+    k_step_t<G, EXACT, BT, TOL><<<gr, kStepThreads, smem, ctx->stream>>>(b, g);
     ctx->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_t launch: %s", cudaGetErrorString(e));
@@ -429,18 +430,18 @@ int launch_step_gram(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     return FC_OK;
 }
 
-template <int CP>
+template <int CP, bool TOL = false>
 int launch_step_wide2(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     static PerDevice<int> grid_pd;
     int& grid = grid_pd(ctx);
     const size_t smem = Wide2Cfg<CP>::smem();
     if (!grid) {
-        CU(cudaFuncSetAttribute(k_step_wide2<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        grid = grid_for((const void*)k_step_wide2<CP>, kW2Threads, smem, ctx->sm_count);
+        CU(cudaFuncSetAttribute(k_step_wide2<CP, TOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_wide2<CP, TOL>, kW2Threads, smem, ctx->sm_count);
     }
     const unsigned long long need = (g.nrows + kW2Rows - 1) / kW2Rows;
     const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
-    k_step_wide2<CP><<<gr, kW2Threads, smem, ctx->stream>>>(b, g);
+    k_step_wide2<CP, TOL><<<gr, kW2Threads, smem, ctx->stream>>>(b, g);
     ctx->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_wide2 launch: %s", cudaGetErrorString(e));
@@ -500,6 +501,8 @@ struct LaunchStep {
         if (g.nrows == 0) return FC_OK;
         if constexpr (S > 1) {
             if (!bt) {
+                if constexpr (S <= 4)
+                    if (ctx->tol) return launch_step_wide2<32 * S, true>(ctx, b, g);
                 if (ctx->step_big) return launch_step_big<32 * S>(ctx, b, g);
                 if constexpr (S <= 4)
                     if (ctx->step_wide2) return launch_step_wide2<32 * S>(ctx, b, g);
@@ -510,6 +513,9 @@ struct LaunchStep {
             // at G = 32 those spill, the lane-parallel k_step below takes bt there)
             if (bt) return g.C == (unsigned)G ? launch_step_t<G, true, true>(ctx, b, g)
                                               : launch_step_t<G, false, true>(ctx, b, g);
+            if (ctx->tol)
+                return g.C == (unsigned)G ? launch_step_t<G, true, false, true>(ctx, b, g)
+                                          : launch_step_t<G, false, false, true>(ctx, b, g);
             return g.C == (unsigned)G ? launch_step_t<G, true, false>(ctx, b, g)
                                       : launch_step_t<G, false, false>(ctx, b, g);
         }
@@ -759,12 +765,14 @@ int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr, unsigned max
     if (TS == 8) R = std::max(8, std::min(16, 2048 / (int)((c + 7) & ~7u)));
     if (const char* e = std::getenv("FC_GRAM_R")) R = std::max(1, std::min(128, std::atoi(e)));
     const size_t smem = gram_smem((int)c, dual ? 1 : 0, R, TS);
-    static PerDevice<size_t[9]> smem_set_pd;
-    size_t (&smem_set)[9] = smem_set_pd(ctx);
-    auto kfn = TS == 1 ? k_gram<1> : (TS == 8 ? k_gram<8> : k_gram<4>);
-    if (smem > 48 * 1024 && smem > smem_set[TS]) {
+    static PerDevice<size_t[18]> smem_set_pd;
+    size_t (&smem_set)[18] = smem_set_pd(ctx);
+    auto kfn = ctx->tol ? (TS == 1 ? k_gram<1, true> : (TS == 8 ? k_gram<8, true> : k_gram<4, true>))
+                        : (TS == 1 ? k_gram<1> : (TS == 8 ? k_gram<8> : k_gram<4>));
+    const int sidx = TS + (ctx->tol ? 9 : 0);
+    if (smem > 48 * 1024 && smem > smem_set[sidx]) {
         CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set[TS] = smem;
+        smem_set[sidx] = smem;
     }
     for (size_t s = 0; s < ctx->shards.size(); ++s) {
         const Geo g = make_geo(ctx, s);
@@ -898,7 +906,12 @@ static int gram_and_sweep(fc_ctx* ctx) {
 }
 
 int enqueue_fista_iteration(fc_ctx* ctx, int bt) {
-    if (fused_step_gram(ctx, bt)) {
+    if (ctx->tol) {                                  // single gather: S X_ext by linearity in the next step
+        TRY(phase_step(ctx, 0));
+        TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
+        TRY(phase_gram(ctx, true));
+        TRY(phase_sweep(ctx, false));
+    } else if (fused_step_gram(ctx, bt)) {
         TRY(phase_step_gram(ctx));
         TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
         TRY(phase_sweep(ctx, true));
@@ -1294,6 +1307,16 @@ int fc_create_loopback(fc_ctx** out, fc_loopback* group, int rank) {
     }
     return rc;
 }
+
+int fc_set_parity_mode(fc_ctx* ctx, int mode) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    if (mode != 0 && mode != 1) return set_err(ctx, FC_INVALID, "parity_mode must be 0 (bitwise) or 1 (tolerance)");
+    if (ctx->session) return set_err(ctx, FC_INVALID, "parity_mode: a solver session is open");
+    ctx->tol = mode == 1;
+    return FC_OK;
+}
+
+int fc_get_parity_mode(const fc_ctx* ctx) { return ctx && ctx->tol ? 1 : 0; }
 
 int fc_create_virtual(fc_ctx** out, int device, int shards) {
     if (shards > 32) return set_err(nullptr, FC_INVALID, "at most 32 virtual shards");
@@ -1771,9 +1794,11 @@ int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const 
     if (bt && !(cfg->bt_eta > 1.0)) return set_err(ctx, FC_INVALID, "solver: backtracking eta must be > 1");
     if (!ctx->have_csr) return set_err(ctx, FC_INVALID, "no similarity uploaded (call fc_upload_csr first)");
     if (c == 0) return set_err(ctx, FC_INVALID, "membership: empty matrix");
+    if (ctx->tol && (bt || c > 128))
+        return set_err(ctx, FC_INVALID, "parity_mode 1 supports GPA and FISTA without backtracking, C <= 128");
     {
         HostPhase hp("ensure_work");
-        TRY(ensure_work(ctx, c, bt));
+        TRY(ensure_work(ctx, c, bt || (ctx->tol && cfg->method == FC_FISTA)));
         // prelude + every trace_every-th iteration + the terminating record
         TRY(ensure_trace(ctx, std::min<uint64_t>(cfg->max_iter / std::max<uint64_t>(cfg->trace_every, 1) + 3,
                                                  1u << 20)));
@@ -1809,6 +1834,9 @@ int fc_solver_begin(fc_ctx* ctx, const fc_solver_config* cfg, uint32_t c, const 
     s.loss_prev = (double)ctx->n * (double)ctx->n;   // GPA: loss^{-1} := N^2 (solver.hpp:149-151)
     s.xs_r = 0;
     s.xs_w = 0;
+    s.tolmode = ctx->tol ? 1 : 0;
+    s.xs_a = 0;
+    s.xs_b = 0;
     TRY(upload_state(ctx, s));
     k_stamp<<<1, 1, 0, ctx->stream>>>(ctx->d_state);   // device clock origin of elapsed_ms
     TRY(check_launch(ctx, "k_stamp"));
@@ -1835,6 +1863,7 @@ static std::vector<char> iteration_key(fc_ctx* ctx) {
     auto put = [&](const void* p, size_t n) { k.insert(k.end(), (const char*)p, (const char*)p + n); };
     put(&ctx->method, sizeof ctx->method);
     put(&ctx->c, sizeof ctx->c);
+    put(&ctx->tol, sizeof ctx->tol);
     for (size_t s = 0; s < ctx->shards.size(); ++s) {
         const Bufs b = make_bufs(ctx, s);
         const Geo g = make_geo(ctx, s);

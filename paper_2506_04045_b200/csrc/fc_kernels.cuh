@@ -77,6 +77,11 @@ struct DevState {
     unsigned long long err_bits;    // validation: max feasibility error (as bits)
     unsigned int nonfinite;
     unsigned int pad;
+    // tolerance mode (fc_set_parity_mode 1): FISTA's S X_ext by linearity from two S bar sweeps
+    int tolmode;
+    int xs_a;                       // xs set holding S bar^{n-1} (read by the step of iteration n)
+    int xs_b;                       // xs set holding S bar^{n-2}
+    int pad_tol;
 };
 
 struct TraceRec {                   // == fc_trace_record
@@ -125,6 +130,12 @@ struct Geo {
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+// acc + a*b: the reference's two roundings (bitwise mode), or one fused rounding (TOL)
+template <bool TOL>
+__device__ __forceinline__ double madd(double acc, double a, double b) {
+    if constexpr (TOL) return __fma_rn(a, b, acc);
+    else return __dadd_rn(acc, __dmul_rn(a, b));
+}
 // std::max(a, b) as the reference uses it: (a < b) ? b : a
 __device__ __forceinline__ double ref_max(double a, double b) { return (a < b) ? b : a; }
 // FISTA extrapolation, solver.hpp:261: b + beta * (b - p)
@@ -974,7 +985,7 @@ __host__ __device__ inline size_t gram_smem(int C, int dual, int R, int TS = 4) 
 // TS x TS register tiles: TS = 4 in general; TS = 1 when there are few 1024-row
 // blocks (small N): every (r, s) pair gets its own thread, so the 1024-long
 // sequential chains of all pairs run in parallel instead of 16 per thread.
-template <int TS>
+template <int TS, bool TOL = false>
 __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dual, int rows_per_chunk) {
     const DevState* st = b.st;
     if (st->done) return;
@@ -1076,7 +1087,7 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
 #pragma unroll
                 for (int a = 0; a < TS; ++a)
 #pragma unroll
-                    for (int c = 0; c < TS; ++c) acc[a][c] = dadd(acc[a][c], dmul(xr[a], xq[c]));
+                    for (int c = 0; c < TS; ++c) acc[a][c] = madd<TOL>(acc[a][c], xr[a], xq[c]);
             }
         }
         __syncthreads();                                     // stage sidx is re-filled next round
@@ -1274,6 +1285,11 @@ __device__ bool finalize_decide(Bufs& b, Geo& g, int kind) {
         if (st->bt) st->frob_gy = frob_g;
         st->xs_r = st->xs_w;                      // S x0 is the first step's S y
         if (st->bt) st->xs_w = 1 - st->xs_w;
+        if (st->tolmode) {                        // single-gather sweeps alternate between two sets
+            st->xs_a = st->xs_w;
+            st->xs_b = st->xs_w;
+            st->xs_w = 1 - st->xs_w;
+        }
         st->iter = 1;
         return true;
     }
@@ -1299,6 +1315,7 @@ __device__ bool finalize_decide(Bufs& b, Geo& g, int kind) {
         st->sw_b = st->step_dst;
         st->loss_prev = loss;
         st->iter = n + 1;
+        if (st->tolmode) st->xs_a = st->xs_w;     // literal step: S bar of this sweep
         return true;
     }
 
@@ -1336,6 +1353,11 @@ __device__ bool finalize_decide(Bufs& b, Geo& g, int kind) {
     const int bar_idx = st->sw_b, prev_idx = st->sw_p;
     st->xs_r = st->xs_w;                          // this pass's S bar / S X_ext feed the next step
     if (st->bt) st->xs_w = 1 - st->xs_w;
+    if (st->tolmode) {                            // S bar^n (this sweep) and S bar^{n-1} (the previous)
+        st->xs_a = st->xs_w;
+        st->xs_b = 1 - st->xs_w;
+        st->xs_w = 1 - st->xs_w;                  // the next sweep overwrites S bar^{n-1} after the step read it
+    }
     if (increased && st->restart) {               // solver.hpp:247-249
         st->t = 1.0;
         st->step_mode = kLiteral;
@@ -1755,7 +1777,8 @@ struct StepPlan {
     const double* A;                                         // bar^{n-1} (or the literal point)
     const double* Bp;                                        // bar^{n-2}
     double* D;                                               // receives bar^n
-    const double* XS;                                        // S X_ext^n (or S bar)
+    const double* XS;                                        // S X_ext^n (or S bar); TOL: S bar^{n-1}
+    const double* XSB;                                       // TOL: S bar^{n-2} (S X_ext^n by linearity)
     double beta, tau;
     int mode;
 };
@@ -1769,7 +1792,13 @@ __device__ __forceinline__ StepPlan step_plan(const Bufs& b) {
     p.D = b.U[st->step_dst];
     p.beta = st->beta_step;
     p.tau = st->tau;
-    p.XS = b.xs[st->xs_r * 2 + st->step_sel];
+    if (st->tolmode) {
+        p.XS = b.xs[st->xs_a * 2];
+        p.XSB = b.xs[st->xs_b * 2];
+    } else {
+        p.XS = b.xs[st->xs_r * 2 + st->step_sel];
+        p.XSB = nullptr;
+    }
     return p;
 }
 
@@ -1788,7 +1817,7 @@ __device__ __forceinline__ void stage_gram_matrix(const Bufs& b, double* Gr, int
 // and TX the new rows bar^n (already stored to D).  Returns false on a non-finite y.
 // BT: also the backtracking row terms (as k_step): lin_i = sum_r g_r (bar_r - x_r),
 // sq_i = sum_r (bar_r - x_r)^2, <xs_i, x_i>; g is parked in the thread's A-tile row.
-template <int G, bool EXACT, bool BT>
+template <int G, bool EXACT, bool BT, bool TOL = false>
 __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, const Geo& g, const double* Gr,
                                              int C, double* TA, double* TB, double* TX, unsigned long long rb,
                                              unsigned long long rend) {
@@ -1844,13 +1873,19 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
 #pragma unroll
                 for (int u = 0; u < KU; ++u) {
                     const double2 gg = reinterpret_cast<const double2*>(Gr + (k0 + u) * G)[l2];
-                    if (EXACT || 2 * l2 < C) o[u] = dadd(o[u], dmul(gg.x, xr[2 * l2]));
-                    if (EXACT || 2 * l2 + 1 < C) o[u] = dadd(o[u], dmul(gg.y, xr[2 * l2 + 1]));
+                    if (EXACT || 2 * l2 < C) o[u] = madd<TOL>(o[u], gg.x, xr[2 * l2]);
+                    if (EXACT || 2 * l2 + 1 < C) o[u] = madd<TOL>(o[u], gg.y, xr[2 * l2 + 1]);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < KU; ++u)
-                if (EXACT || k0 + u < C) tr[k0 + u] = dmul(-4.0, dsub(tr[k0 + u], o[u]));
+            for (int u = 0; u < KU; ++u) {
+                if (EXACT || k0 + u < C) {
+                    double xsv = tr[k0 + u];
+                    if constexpr (TOL)                       // S X_ext = S bar + beta (S bar - S bar_prev)
+                        if (mode != kLiteral) xsv = extrap(xsv, ldg(sp.XSB + (size_t)(rb + lane) * C + k0 + u), sp.beta);
+                    tr[k0 + u] = dmul(-4.0, dsub(xsv, o[u]));
+                }
+            }
         }
         // y = x - tau * grad (solver.hpp:102)
         bool fin = true;
@@ -1903,7 +1938,7 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
     return !bad;
 }
 
-template <int G, bool EXACT, bool BT = false>
+template <int G, bool EXACT, bool BT = false, bool TOL = false>
 __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
     DevState* st = b.st;
     if (st->done) return;
@@ -1922,7 +1957,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
     const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
     bool ok = true;
     for (unsigned long long rb = w0 * 32; rb < g.nrows; rb += warps * 32)
-        ok = step_t_batch<G, EXACT, BT>(sp, b, g, Gr, C, TA, TB, TX, rb, g.nrows) && ok;
+        ok = step_t_batch<G, EXACT, BT, TOL>(sp, b, g, Gr, C, TA, TB, TX, rb, g.nrows) && ok;
     if (!ok) {
         st->error = 1;
         st->done = 1;
@@ -2479,7 +2514,7 @@ struct Wide2Cfg {
     static size_t smem() { return sizeof(double) * ((size_t)CP * CP + (size_t)2 * kW2Rows * LD); }
 };
 
-template <int CP>
+template <int CP, bool TOL = false>
 __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
     DevState* st = b.st;
     if (st->done) return;
@@ -2554,7 +2589,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < KT; ++j) o[i][j] = dadd(o[i][j], dmul(gv[j], xv[i]));
+                    for (int j = 0; j < KT; ++j) o[i][j] = madd<TOL>(o[i][j], gv[j], xv[i]);
             }
         }
         // 3: grad and step, in place of xs
@@ -2565,7 +2600,10 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             for (int j = 0; j < KT; ++j) {
                 const int k = KT * kg + j;
                 if (r < rows && k < C) {
-                    const double grad = dmul(-4.0, dsub(TY[r * LD + k], o[i][j]));
+                    double xsv = TY[r * LD + k];
+                    if constexpr (TOL)
+                        if (sp.mode != kLiteral) xsv = extrap(xsv, ldg(sp.XSB + (size_t)(rb + r) * C + k), sp.beta);
+                    const double grad = dmul(-4.0, dsub(xsv, o[i][j]));
                     TY[r * LD + k] = dsub(TX[r * LD + k], dmul(sp.tau, grad));
                 }
             }
