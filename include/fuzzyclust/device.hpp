@@ -45,6 +45,14 @@ inline Context& context() {
     return c;
 }
 
+/// Second context for operators that only need N (share_matrix / cross_share of an X
+/// whose size differs from the resident similarity): it holds an N-node identity
+/// pattern, so the caller's resident similarity on context() is never evicted.
+inline Context& aux_context() {
+    static Context c;
+    return c;
+}
+
 inline std::uint64_t next_id() {
     static std::uint64_t id = 0;
     return ++id;

@@ -8,11 +8,14 @@
 #pragma once
 
 #include <cmath>
+#include <cstdint>
+#include <cstring>
 #include <span>
 #include <vector>
 
 #include "fuzzyclust/common.hpp"
 #include "fuzzyclust/dense.hpp"
+#include "fuzzyclust/dense_oracle.hpp"
 #include "fuzzyclust/device.hpp"
 #include "fuzzyclust/parallel.hpp"
 #include "fuzzyclust/sparse.hpp"
@@ -59,29 +62,57 @@ private:
 };
 
 namespace detail {
-/// Make an N-node similarity resident when only N matters (share_matrix).
-inline void ensure_size(std::size_t n) {
-    static SparseSimilarity ident;
-    if (ident.size() != n) {
+/// The context an N-only operator (Gram) runs on: the main one when its resident
+/// similarity has N nodes, else the auxiliary one with an N-node identity pattern
+/// (the main context's resident similarity stays where it is).
+inline device::Context& context_for_size(std::size_t n) {
+    auto& d = device::context();
+    if (d.resident != 0 && d.resident_n == n) return d;
+    auto& a = device::aux_context();
+    if (a.resident_n != n || a.resident == 0) {
         std::vector<std::int64_t> rp(n + 1);
         std::vector<std::uint32_t> ci(n);
         for (std::size_t i = 0; i <= n; ++i) rp[i] = static_cast<std::int64_t>(i);
         for (std::size_t i = 0; i < n; ++i) ci[i] = static_cast<std::uint32_t>(i);
-        ident = SparseSimilarity::from_csr(n, std::move(rp), std::move(ci), {}, false);
+        device::check(fc_upload_csr(a.ctx, n, n, rp.data(), ci.data(), nullptr, static_cast<double>(n)), a.ctx);
+        a.resident = device::next_id();
+        a.resident_n = n;
     }
-    ident.ensure_resident();
+    return a;
 }
-inline bool resident_size_is(std::size_t n) {
-    const auto& d = device::context();
-    return d.resident != 0 && d.resident_n == n;
+
+/// 64-bit fingerprint of X's contents (every bit of every entry, order-sensitive).
+inline std::uint64_t content_fingerprint(std::span<const double> v) {
+    std::uint64_t h = 0x9E3779B97F4A7C15ULL ^ v.size();
+    for (double e : v) {
+        std::uint64_t u;
+        std::memcpy(&u, &e, sizeof u);
+        h = (h ^ u) * 0x100000001B3ULL;
+        h ^= h >> 29;
+    }
+    return h;
+}
+
+/// The last device sweep, reused while (similarity, X) are unchanged: a reference-style
+/// loop over columns (similarity_column_product / gradient_column / loss_terms_column
+/// for i = 0..N-1) then costs one sweep plus an O(N C) host fingerprint per call,
+/// not one O(nnz) sweep and an N x C upload per column.
+struct SweepCache {
+    std::uint64_t sim = 0, fp = 0;
+    std::size_t rows = 0, cols = 0;
+    std::vector<double> xs;
+    double merge = 0.0;
+};
+inline SweepCache& sweep_cache() {
+    static SweepCache c;
+    return c;
 }
 }  // namespace detail
 
 /// X X^T (objective.hpp:92-95) on the device, 1024-column blocks combined in order.
 inline ShareMatrix share_matrix(const DenseMatrix& x, unsigned /*workers*/ = 1) {
-    if (!detail::resident_size_is(x.cols())) detail::ensure_size(x.cols());
+    auto& d = detail::context_for_size(x.cols());
     ShareMatrix out(x.rows());
-    auto& d = device::context();
     device::check(fc_share_matrix(d.ctx, static_cast<uint32_t>(x.rows()), x.data().data(), out.raw()), d.ctx);
     return out;
 }
@@ -90,9 +121,8 @@ inline ShareMatrix share_matrix(const DenseMatrix& x, unsigned /*workers*/ = 1) 
 /// the stacked N x 2C matrix [A | B] -- same per-entry products, same block order.
 inline ShareMatrix cross_share(const DenseMatrix& a, const DenseMatrix& b, unsigned /*workers*/ = 1) {
     if (a.rows() != b.rows() || a.cols() != b.cols()) throw InvalidInput("cross_share: shape mismatch");
-    if (!detail::resident_size_is(a.cols())) detail::ensure_size(a.cols());
+    auto& d = detail::context_for_size(a.cols());
     ShareMatrix out(a.rows());
-    auto& d = device::context();
     device::check(fc_cross_share(d.ctx, static_cast<uint32_t>(a.rows()), a.data().data(), b.data().data(), out.raw()),
                   d.ctx);
     return out;
@@ -115,11 +145,35 @@ inline ColumnPass fused_column_pass(const DenseMatrix& x, const SparseSimilarity
     return p;
 }
 
-/// objective.hpp:98-109 (one column: runs the device sweep, O(nnz) per call).
+/// objective.hpp:98-109.  One column of the device sweep; the sweep of (s, x) is cached
+/// (detail::SweepCache), so looping over all columns runs it once.
 inline void similarity_column_product(const DenseMatrix& x, const SparseSimilarity& s, std::size_t i,
                                       std::span<double> out) {
+    if (s.size() != x.cols()) throw InvalidInput("objective: similarity/membership size mismatch");
+    auto& c = detail::sweep_cache();
+    const std::uint64_t fp = detail::content_fingerprint(x.data());
+    if (c.sim != s.device_id() || c.fp != fp || c.rows != x.rows() || c.cols != x.cols()) {
+        ColumnPass p = fused_column_pass(x, s);
+        c.xs = std::move(p.xs);
+        c.merge = p.merge;
+        c.sim = s.device_id();
+        c.fp = fp;
+        c.rows = x.rows();
+        c.cols = x.cols();
+    }
+    for (std::size_t k = 0; k < x.rows(); ++k) out[k] = c.xs[i * x.rows() + k];
+}
+
+/// Batched form (new): X s_i for every i in `cols`, one device sweep; C x |cols| column-major.
+inline std::vector<double> similarity_column_products(const DenseMatrix& x, const SparseSimilarity& s,
+                                                      std::span<const std::size_t> cols) {
     const ColumnPass p = fused_column_pass(x, s);
-    for (std::size_t k = 0; k < x.rows(); ++k) out[k] = p.xs[i * x.rows() + k];
+    std::vector<double> out(x.rows() * cols.size());
+    for (std::size_t j = 0; j < cols.size(); ++j) {
+        if (cols[j] >= x.cols()) throw InvalidInput("objective: column index out of range");
+        for (std::size_t k = 0; k < x.rows(); ++k) out[j * x.rows() + k] = p.xs[cols[j] * x.rows() + k];
+    }
+    return out;
 }
 
 /// objective.hpp:113-118
@@ -127,6 +181,19 @@ inline void gradient_column_fused(const ShareMatrix& share, std::span<const doub
                                   std::span<double> out) {
     auto& d = device::context();
     device::check(fc_gradient_rows(d.ctx, static_cast<uint32_t>(share.dim()), 1, share.raw(), xs_i.data(), x_i.data(),
+                                   out.data()),
+                  d.ctx);
+}
+
+/// Batched form (new): gradient_column_fused for m columns at once (xs, x, out: C x m
+/// column-major), one launch.
+inline void gradient_columns_fused(const ShareMatrix& share, std::span<const double> xs, std::span<const double> x,
+                                   std::span<double> out) {
+    const std::size_t c = share.dim();
+    if (c == 0 || xs.size() != x.size() || out.size() != x.size() || x.size() % c)
+        throw InvalidInput("gradient_columns_fused: shape mismatch");
+    auto& d = device::context();
+    device::check(fc_gradient_rows(d.ctx, static_cast<uint32_t>(c), x.size() / c, share.raw(), xs.data(), x.data(),
                                    out.data()),
                   d.ctx);
 }
@@ -145,6 +212,16 @@ inline double loss_terms_column(std::span<const double> xs_i, std::span<const do
     double out = 0.0;
     auto& d = device::context();
     device::check(fc_loss_terms_rows(d.ctx, static_cast<uint32_t>(x_i.size()), 1, xs_i.data(), x_i.data(), &out),
+                  d.ctx);
+    return out;
+}
+
+/// Batched form (new): loss_terms_column for m columns (C x m column-major), one launch.
+inline std::vector<double> loss_terms_columns(std::size_t c, std::span<const double> xs, std::span<const double> x) {
+    if (c == 0 || xs.size() != x.size() || x.size() % c) throw InvalidInput("loss_terms_columns: shape mismatch");
+    std::vector<double> out(x.size() / c);
+    auto& d = device::context();
+    device::check(fc_loss_terms_rows(d.ctx, static_cast<uint32_t>(c), out.size(), xs.data(), x.data(), out.data()),
                   d.ctx);
     return out;
 }

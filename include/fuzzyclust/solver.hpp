@@ -89,9 +89,8 @@ inline double resolve_step_size(const SolverConfig& config, const SparseSimilari
 /// solver.hpp:89-107 (one projected-gradient update from precomputed X s_i).
 inline MembershipMatrix gpa_step_fused(const MembershipMatrix& x, const ShareMatrix& share,
                                        const std::vector<double>& xs, double tau, unsigned /*workers*/ = 1) {
-    if (!detail::resident_size_is(x.nodes())) detail::ensure_size(x.nodes());
+    auto& d = detail::context_for_size(x.nodes());
     MembershipMatrix next(x.clusters(), x.nodes());
-    auto& d = device::context();
     device::check(fc_gpa_step_fused(d.ctx, static_cast<uint32_t>(x.clusters()), x.data().data(), share.raw(),
                                     xs.data(), tau, next.data().data()),
                   d.ctx);

@@ -79,3 +79,38 @@ def build_dropin_test(force: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+
+
+REF_TESTS = os.environ.get("FC_REF_TESTS", "/root/reference/proj/tests")
+REF_SUITES = ("simplex", "objective", "solver", "secondorder", "graph")
+SHIM = os.path.join(ROOT, "tests", "cpp", "gtest_shim")
+
+
+def ref_suite_bin(name: str) -> str:
+    return os.path.join(ROOT, "tests", "cpp", "_build", f"ref_{name}_test")
+
+
+def build_reference_suites(force: bool = False) -> list:
+    """The reference's own GTest suites ({simplex,objective,solver,secondorder,graph}_test.cpp
+    + support.hpp),
+    compiled UNMODIFIED from where they lie under /root/reference against the drop-in
+    headers (include/fuzzyclust) and the GoogleTest shim (tests/cpp/gtest_shim), linked to
+    the CUDA library.  Nothing is copied into the repo; without /root/reference (the GPU
+    box) the binaries built here are used as they are."""
+    out = []
+    if not os.path.isdir(REF_TESTS):
+        return [ref_suite_bin(n) for n in REF_SUITES if os.path.exists(ref_suite_bin(n))]
+    hdrs = [os.path.join(ROOT, "include", "fuzzyclust", f) for f in os.listdir(os.path.join(ROOT, "include", "fuzzyclust"))]
+    hdrs += [os.path.join(SHIM, "gtest", "gtest.h"), os.path.join(SHIM, "gtest_main.cpp"), LIB]
+    os.makedirs(os.path.join(ROOT, "tests", "cpp", "_build"), exist_ok=True)
+    for name in REF_SUITES:
+        src = os.path.join(REF_TESTS, f"{name}_test.cpp")
+        dst = ref_suite_bin(name)
+        deps = hdrs + [src, os.path.join(REF_TESTS, "support.hpp")]
+        if force or not os.path.exists(dst) or any(os.path.getmtime(d) > os.path.getmtime(dst) for d in deps):
+            cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I" + os.path.join(ROOT, "include"), "-I" + SHIM,
+                   src, os.path.join(SHIM, "gtest_main.cpp"), "-L" + LIBDIR, "-lfuzzyclust_cuda",
+                   "-Wl,-rpath," + LIBDIR, "-lpthread", "-o", dst]
+            subprocess.run(cmd, check=True)
+        out.append(dst)
+    return out

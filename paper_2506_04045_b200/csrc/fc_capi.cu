@@ -131,6 +131,7 @@ struct fc_ctx {
     double* d_spart = nullptr;
     double* d_totals = nullptr;        // (vshards + 1) slots
     double* d_chain_in = nullptr;
+    char* d_rows_scratch = nullptr;    // fc_gradient_rows / fc_loss_terms_rows staging
     double* d_gfull[2] = {nullptr, nullptr};
     unsigned* d_counter = nullptr;    // [0, 64): row-chunk schedulers per shard; [64, 128): heavy-row schedulers
     unsigned* d_heavy = nullptr;      // per shard: local rows of degree >= heavy_deg, by degree descending
@@ -1345,6 +1346,7 @@ void fc_destroy(fc_ctx* ctx) {
     dfree(ctx, &ctx->d_spart);
     dfree(ctx, &ctx->d_totals);
     dfree(ctx, &ctx->d_chain_in);
+    dfree(ctx, &ctx->d_rows_scratch);
     dfree(ctx, &ctx->d_counter);
     dfree(ctx, &ctx->d_state);
     dfree(ctx, &ctx->d_trace);
@@ -1724,8 +1726,8 @@ int fc_project_simplex_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, double* x) {
     if (c > 256) return set_err(ctx, FC_INVALID, "cluster count C=%u exceeds the supported maximum 256", c);
     if (rows == 0) return FC_OK;
     CU(cudaSetDevice(ctx->device));
-    double* d = nullptr;
-    CU(cudaMallocAsync(&d, rows * c * sizeof(double), ctx->stream));
+    TRY(dalloc(ctx, &ctx->d_rows_scratch, rows * c * sizeof(double)));
+    double* d = reinterpret_cast<double*>(ctx->d_rows_scratch);
     CU(cudaMemcpyAsync(d, x, rows * c * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemsetAsync(ctx->d_counter + 63, 0, sizeof(unsigned), ctx->stream));
     int rc = by_c<LaunchProject>(ctx, c, ctx, d, (unsigned long long)rows, (int)c, ctx->d_counter + 63);
@@ -1734,7 +1736,6 @@ int fc_project_simplex_rows(fc_ctx* ctx, uint32_t c, uint64_t rows, double* x) {
         CU(cudaMemcpyAsync(x, d, rows * c * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaMemcpyAsync(&bad, ctx->d_counter + 63, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     }
-    CU(cudaFreeAsync(d, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     if (rc) return rc;
     if (bad) return set_err(ctx, FC_INVALID, "project_simplex: non-finite entry");
@@ -1750,8 +1751,10 @@ static int rows_kernel(fc_ctx* ctx, uint32_t c, uint64_t rows, const double* g, 
     const size_t vb = rows * c * sizeof(double);
     const size_t gb = gradient ? (size_t)c * c * sizeof(double) : 0;
     const size_t ob = gradient ? vb : rows * sizeof(double);
-    char* d = nullptr;
-    CU(cudaMallocAsync(reinterpret_cast<void**>(&d), gb + 2 * vb + ob, ctx->stream));
+    // grow-only scratch owned by the context (a per-call cudaMallocAsync made a
+    // reference-style loop over columns pay an allocation per column)
+    TRY(dalloc(ctx, &ctx->d_rows_scratch, gb + 2 * vb + ob));
+    char* d = ctx->d_rows_scratch;
     double* dg = reinterpret_cast<double*>(d);
     double* dxs = reinterpret_cast<double*>(d + gb);
     double* dx = reinterpret_cast<double*>(d + gb + vb);
@@ -1764,7 +1767,6 @@ static int rows_kernel(fc_ctx* ctx, uint32_t c, uint64_t rows, const double* g, 
     else k_loss_terms_rows<<<blocks, 128, 0, ctx->stream>>>(dxs, dx, dout, rows, (int)c);
     TRY(check_launch(ctx, gradient ? "k_gradient_rows" : "k_loss_terms_rows"));
     TRY(d2h(ctx, out, dout, ob));
-    CU(cudaFreeAsync(d, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return FC_OK;
 }

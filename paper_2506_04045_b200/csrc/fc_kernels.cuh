@@ -1845,7 +1845,11 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
             const int t = (p + sub) * LD + lg;
             cp_async8(TA + t, A + a);
             if (mode != kLiteral) cp_async8(TB + t, Bp + a);
-            cp_async8(TX + t, XS + (size_t)row * C + lg);
+            const size_t q = (size_t)row * C + lg;
+            if (TOL && mode != kLiteral)                     // S X_ext = S bar + beta (S bar - S bar_prev)
+                TX[t] = extrap(ldg(XS + q), ldg(sp.XSB + q), sp.beta);
+            else
+                cp_async8(TX + t, XS + q);
         }
     }
     cp_async_commit();
@@ -1879,12 +1883,7 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
             }
 #pragma unroll
             for (int u = 0; u < KU; ++u) {
-                if (EXACT || k0 + u < C) {
-                    double xsv = tr[k0 + u];
-                    if constexpr (TOL)                       // S X_ext = S bar + beta (S bar - S bar_prev)
-                        if (mode != kLiteral) xsv = extrap(xsv, ldg(sp.XSB + (size_t)(rb + lane) * C + k0 + u), sp.beta);
-                    tr[k0 + u] = dmul(-4.0, dsub(xsv, o[u]));
-                }
+                if (EXACT || k0 + u < C) tr[k0 + u] = dmul(-4.0, dsub(tr[k0 + u], o[u]));
             }
         }
         // y = x - tau * grad (solver.hpp:102)
@@ -2511,7 +2510,7 @@ struct Wide2Cfg {
     static constexpr int LD = CP + 1;
     static constexpr int KT = CP / 32;                      // k per thread in the GEMM
     static constexpr int VPL = CP / 8;                      // values per lane in the projection
-    static size_t smem() { return sizeof(double) * ((size_t)CP * CP + (size_t)2 * kW2Rows * LD); }
+    static size_t smem() { return sizeof(double) * ((size_t)CP * CP + (size_t)3 * kW2Rows * LD); }
 };
 
 template <int CP, bool TOL = false>
@@ -2526,8 +2525,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
     double* GS = smw2;                                       // GS[l*CP + k] = G[k][l]
     double* TX = GS + CP * CP;
     double* TY = TX + R * LD;
-    __shared__ double thr_s[R];
-    __shared__ int work_s[R];
+    double* CS = TY + R * LD;                                // running sums of the sorted rows
     const int C = (int)g.C;
     const int tid = threadIdx.x;
     const StepPlan sp = step_plan(b);
@@ -2546,21 +2544,42 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
          rb += (unsigned long long)gridDim.x * R) {
         const int rows = (int)min((unsigned long long)R, g.nrows - rb);
         __syncthreads();                                     // previous batch's tiles consumed (and GS staged)
-        // 1: X_ext rows (registers -> TX), S X_ext rows -> TY
+        // 1: A -> TX, B -> TY (cp.async), X_ext formed in place in TX (solver.hpp:261), then
+        //    S X_ext -> TY, which lands while the GEMM runs (it is read only after it)
+#pragma unroll 4
         for (int e = tid; e < R * CP; e += kW2Threads) {
             const int r = e / CP, k = e % CP;
-            double xv = 0.0;
             if (r < rows && k < C) {
                 const size_t a = (size_t)(g.row0 + rb + r) * C + k;
-                const double av = ldg(sp.A + a);
-                xv = (sp.mode == kLiteral) ? av : extrap(av, ldg(sp.Bp + a), sp.beta);
-                cp_async8(TY + r * LD + k, sp.XS + (size_t)(rb + r) * C + k);
+                cp_async8(TX + r * LD + k, sp.A + a);
+                if (sp.mode != kLiteral) cp_async8(TY + r * LD + k, sp.Bp + a);
+            } else {
+                TX[r * LD + k] = 0.0;                        // padding: x_l = 0 beyond C
             }
-            TX[r * LD + k] = xv;
         }
         cp_async_commit();
         cp_async_wait_all();
         __syncthreads();
+        if (sp.mode != kLiteral) {
+#pragma unroll 4
+            for (int e = tid; e < rows * CP; e += kW2Threads) {
+                const int r = e / CP, k = e % CP;
+                if (k < C) TX[r * LD + k] = extrap(TX[r * LD + k], TY[r * LD + k], sp.beta);
+            }
+            __syncthreads();
+        }
+#pragma unroll 4
+        for (int e = tid; e < rows * CP; e += kW2Threads) {
+            const int r = e / CP, k = e % CP;
+            if (k < C) {
+                const size_t q = (size_t)(rb + r) * C + k;
+                if (TOL && sp.mode != kLiteral)              // S X_ext = S bar + beta (S bar - S bar_prev)
+                    TY[r * LD + k] = extrap(ldg(sp.XS + q), ldg(sp.XSB + q), sp.beta);
+                else
+                    cp_async8(TY + r * LD + k, sp.XS + q);
+            }
+        }
+        cp_async_commit();
         // 2: GEMM
         double o[4][KT];
 #pragma unroll
@@ -2593,6 +2612,8 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             }
         }
         // 3: grad and step, in place of xs
+        cp_async_wait_all();
+        __syncthreads();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int r = 4 * rg + i;
@@ -2600,16 +2621,14 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             for (int j = 0; j < KT; ++j) {
                 const int k = KT * kg + j;
                 if (r < rows && k < C) {
-                    double xsv = TY[r * LD + k];
-                    if constexpr (TOL)
-                        if (sp.mode != kLiteral) xsv = extrap(xsv, ldg(sp.XSB + (size_t)(rb + r) * C + k), sp.beta);
-                    const double grad = dmul(-4.0, dsub(xsv, o[i][j]));
+                    const double grad = dmul(-4.0, dsub(TY[r * LD + k], o[i][j]));
                     TY[r * LD + k] = dsub(TX[r * LD + k], dmul(sp.tau, grad));
                 }
             }
         }
         __syncthreads();
-        // 4a: 8 lanes per row: finiteness, register bitonic sort (descending) -> TX
+        // 4: projection, warp-local: warp w owns rows 4w..4w+3, 8 lanes per row
+        // 4a: finiteness, register bitonic sort (descending) -> TX (x is dead)
         const bool live = pr < rows;
         double v[VPL];
         bool fin = true;
@@ -2653,60 +2672,75 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
                 }
             }
         }
+        double* srow = TX + pr * LD;                         // sorted values
+        double* crow = CS + pr * LD;                         // their running sums
+        double* yrow = TY + pr * LD;
 #pragma unroll
-        for (int m = 0; m < VPL; ++m) TX[pr * LD + VPL * pq + m] = v[m];
-        if (pq == 0) work_s[pr] = work ? 1 : 0;
-        __syncthreads();
-        // 4b: one thread per row: sequential cumsum / threshold (simplex.hpp:29-36)
-        if (tid < R) {
-            const int r = tid;
-            double thr = 0.0;
-            if (work_s[r]) {
-                const double* sr = TX + r * LD;
-                double cs = 0.0, a_star = 0.0;
-                int k_star = -1;
-                for (int k = 0; k < C; ++k) {
-                    const double sk = sr[k];
-                    cs = dadd(cs, sk);
-                    const double a = dsub(cs, 1.0);
-                    if (threshold_cond(sk, a, (double)(k + 1))) {
-                        k_star = k;
-                        a_star = a;
-                    }
-                }
-                thr = k_star >= 0 ? a_star / (double)(k_star + 1) : 0.0;
+        for (int m = 0; m < VPL; ++m) srow[VPL * pq + m] = v[m];
+        __syncwarp();
+        // 4b: the only sequential part of the threshold (simplex.hpp:29-36): cs_k = cs_{k-1} + s_k,
+        //     one lane per row; the tests then run on all 8 lanes of the row
+        if (pq == 0 && work) {
+            double cs = 0.0;
+            for (int k = 0; k < C; ++k) {
+                cs = dadd(cs, srow[k]);
+                crow[k] = cs;
             }
-            thr_s[r] = thr;
         }
-        __syncthreads();
-        // 4c: clip (every lane its slots)
+        __syncwarp();
+        int kbest = -1;                                      // last k whose test holds
         if (work) {
-            const double thr = thr_s[pr];
 #pragma unroll
             for (int m = 0; m < VPL; ++m) {
                 const int k = VPL * pq + m;
-                if (k < C) TY[pr * LD + k] = ref_max(dsub(TY[pr * LD + k], thr), 0.0);
+                if (k < C && threshold_cond(srow[k], dsub(crow[k], 1.0), (double)(k + 1))) kbest = k;
+            }
+        }
+#pragma unroll
+        for (int o2 = 1; o2 < 8; o2 <<= 1) kbest = max(kbest, __shfl_xor_sync(gmask, kbest, o2));
+        if (work) {
+            const double thr = kbest >= 0 ? dsub(crow[kbest], 1.0) / (double)(kbest + 1) : 0.0;
+#pragma unroll
+            for (int m = 0; m < VPL; ++m) {                  // 4c: clip
+                const int k = VPL * pq + m;
+                if (k < C) yrow[k] = ref_max(dsub(yrow[k], thr), 0.0);
             }
         } else if (live && row_fin && C == 1 && pq == 0) {
-            TY[pr * LD] = 1.0;
+            yrow[0] = 1.0;
         }
-        __syncthreads();
-        // 4d: residual folds (simplex.hpp:43-55), one thread per row, index order
-        if (tid < R && work_s[tid]) {
-            double* ty = TY + tid * LD;
-            for (int round = 0; round < 4; ++round) {
+        __syncwarp();
+        // 4d: residual folds (simplex.hpp:43-55): the sum in index order by one lane, max /
+        //     ties / update on the 8 lanes
+        for (int round = 0; round < 4; ++round) {
+            double residual = 0.0;
+            if (pq == 0 && work) {
                 double sum = 0.0;
-                for (int k = 0; k < C; ++k) sum = dadd(sum, ty[k]);
-                const double residual = dsub(sum, 1.0);
-                if (residual == 0.0) break;
-                double top = ty[0];
-                for (int k = 1; k < C; ++k) top = (top < ty[k]) ? ty[k] : top;
-                int ties = 0;
-                for (int k = 0; k < C; ++k) ties += (ty[k] == top);
-                const double share = residual / (double)ties;
-                for (int k = 0; k < C; ++k)
-                    if (ty[k] == top) ty[k] = ref_max(dsub(ty[k], share), 0.0);
+                for (int k = 0; k < C; ++k) sum = dadd(sum, yrow[k]);
+                residual = dsub(sum, 1.0);
             }
+            residual = __shfl_sync(gmask, residual, (tid & 31) & ~7);
+            const bool go = work && residual != 0.0;
+            if (!__any_sync(0xffffffffu, go)) break;
+            double top = -INFINITY;
+            if (go)
+                for (int k = pq; k < C; k += 8) top = (top < yrow[k]) ? yrow[k] : top;
+#pragma unroll
+            for (int o2 = 1; o2 < 8; o2 <<= 1) {
+                const double t2 = __shfl_xor_sync(gmask, top, o2);
+                top = (top < t2) ? t2 : top;
+            }
+            int ties = 0;
+            if (go)
+                for (int k = pq; k < C; k += 8) ties += (yrow[k] == top);
+#pragma unroll
+            for (int o2 = 1; o2 < 8; o2 <<= 1) ties += __shfl_xor_sync(gmask, ties, o2);
+            __syncwarp();
+            if (go) {
+                const double share = residual / (double)ties;
+                for (int k = pq; k < C; k += 8)
+                    if (yrow[k] == top) yrow[k] = ref_max(dsub(yrow[k], share), 0.0);
+            }
+            __syncwarp();
         }
         __syncthreads();
         // 5: store bar^n

@@ -48,3 +48,29 @@ def test_dropin_traces_match_reference_goldens(binary):
         x = np.array([float.fromhex(v) for v in mem.split()]).reshape(7, 2)
         want = np.array([[float.fromhex(v) for v in row] for row in g["membership"]])
         assert np.array_equal(x, want), name
+
+
+# ---- the reference's own GTest suites, compiled unmodified against include/ -----------------
+@pytest.fixture(scope="module")
+def ref_suites():
+    bins = fcbuild.build_reference_suites()
+    if len(bins) != len(fcbuild.REF_SUITES):
+        pytest.skip("reference suites not built (needs /root/reference at build time)")
+    return dict(zip(fcbuild.REF_SUITES, bins))
+
+
+def test_reference_suites_link_cuda_library(ref_suites):
+    for name, b in ref_suites.items():
+        out = subprocess.run(["ldd", b], capture_output=True, text=True).stdout
+        assert "libfuzzyclust_cuda.so" in out, name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", ["simplex", "objective", "solver", "secondorder", "graph"])
+def test_reference_suite_passes_against_dropin(ref_suites, suite):
+    """/root/reference/proj/tests/<suite>_test.cpp (+ support.hpp), unmodified, through the
+    drop-in headers on the device: every TEST of the reference passes."""
+    r = subprocess.run([ref_suites[suite]], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-2000:]
+    assert "[  FAILED  ]" not in r.stdout
