@@ -39,6 +39,9 @@ CONFIGS = {
     "A": dict(kind="sbm", n=10_000, m=202_800, c=8, blocks=8, method="gpa"),
     "B": dict(kind="sbm", n=1_000_000, m=20_010_000, c=16, blocks=16, method="fista_bt"),
     "C": dict(kind="citation", n=10_000_000, m=206_100_000, c=32, method="fista"),
+    # config C with the locality knob on (ids in citation time order: neighbours near in id
+    # space -- L2-friendly gathers on one GPU, halo exchange instead of allgather on N GPUs)
+    "Cloc": dict(kind="citation", n=10_000_000, m=206_100_000, c=32, method="fista", locality=True),
     "D": dict(kind="citation", n=70_000_000, m=1_032_000_000, c=32, method="fista"),
     "E8": dict(kind="citation", n=4_000_000, m=82_500_000, c=8, method="fista"),
     "E32": dict(kind="citation", n=4_000_000, m=82_500_000, c=32, method="fista"),
@@ -297,7 +300,7 @@ def run_reference_arm(args, cfg):
 
 def config_name(name, cfg):
     return (f"config {name}: {cfg['kind']} n={cfg['n']}, {cfg['m']} edge draws, k={cfg['c']}, "
-            f"{cfg['method'].upper()}")
+            f"{cfg['method'].upper()}" + (", locality on" if cfg.get("locality") else ""))
 
 
 def main():
@@ -547,6 +550,7 @@ def main():
             "config": {"workload": config_name(args.config, cfg), "n": graph.n, "nnz": graph.nnz,
                        "edges_undirected": (graph.nnz - graph.n) // 2, "k": cfg["c"],
                        "parallelism": f"rows{world}", "l2": "inputs >> 126 MB L2 (no flush needed)",
+                       "exchange": ("halo" if ctx.halo_info()[0] else "allgather") if world > 1 else None,
                        "graph_gen_s": round(t_graph, 1)},
             "edges_per_s": graph.nnz * value,
             "achieved_gbs": it_b_total * value / 1e9,

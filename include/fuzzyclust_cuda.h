@@ -104,6 +104,12 @@ int fc_create_virtual(fc_ctx** out, int device, int shards);
 int fc_set_parity_mode(fc_ctx* ctx, int mode);
 int fc_get_parity_mode(const fc_ctx* ctx);
 
+/* Multi-rank exchange plan chosen at fc_upload_csr: 1 = halo exchange (only the rows
+ * other shards' columns name move each iteration; locality graphs), 0 = full
+ * allgather.  FC_HALO=0/1 forces it; default: halo when every rank then receives less
+ * than half of what the allgather would move.  Rows received / sent per exchange. */
+int fc_halo_info(const fc_ctx* ctx, uint64_t* recv_rows, uint64_t* send_rows);
+
 /* In-process loopback group (tests / single-GPU validation of the multi-rank path):
  * `world` rank contexts in ONE process on `device`, one host thread per rank, each
  * created with fc_create_loopback.  The collectives are stream-ordered device copies

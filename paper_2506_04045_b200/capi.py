@@ -63,6 +63,7 @@ SIGNATURES = {
     "fc_create_virtual": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int]),
     "fc_set_parity_mode": (C.c_int, [C.c_void_p, C.c_int]),
     "fc_get_parity_mode": (C.c_int, [C.c_void_p]),
+    "fc_halo_info": (C.c_int, [C.c_void_p, _u64p, _u64p]),
     "fc_loopback_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int]),
     "fc_loopback_destroy": (None, [C.c_void_p]),
     "fc_create_loopback": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int]),
@@ -240,6 +241,12 @@ class Context:
 
     def parity_mode(self) -> int:
         return int(lib().fc_get_parity_mode(self.h))
+
+    def halo_info(self):
+        """(halo_mode, rows received per exchange, rows sent per exchange)."""
+        r, s = C.c_uint64(), C.c_uint64()
+        mode = lib().fc_halo_info(self.h, C.byref(r), C.byref(s))
+        return int(mode), int(r.value), int(s.value)
 
     def close(self):
         if getattr(self, "h", None):

@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -58,8 +59,9 @@ struct HostPhase {
         static const bool v = [] { const char* e = std::getenv("FC_TRACE_HOST"); return e && *e == '1'; }();
         return v;
     }
-    explicit HostPhase(const char* n) : name(n), t0(std::chrono::steady_clock::now()) {}
+    explicit HostPhase(const char* n) : name(n), t0(std::chrono::steady_clock::now()) { nvtxRangePushA(n); }
     ~HostPhase() {
+        nvtxRangePop();
         if (on())
             std::fprintf(stderr, "[fc] %-22s %8.2f ms\n", name,
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
@@ -132,6 +134,17 @@ struct fc_ctx {
     double* d_totals = nullptr;        // (vshards + 1) slots
     double* d_chain_in = nullptr;
     char* d_rows_scratch = nullptr;    // fc_gradient_rows / fc_loss_terms_rows staging
+    // halo exchange (multi-rank, locality graphs): only the rows a peer's shard references
+    bool halo = false;
+    int halo_mode = -1;                // FC_HALO: 0 off, 1 on, -1 auto (when it moves < half the allgather)
+    std::vector<uint64_t> halo_send_off, halo_recv_off, halo_peer_off;   // doubles, world + 1 (peer: world)
+    unsigned* d_halo_send_rows = nullptr;   // own rows to pack, grouped by destination
+    unsigned* d_halo_recv_rows = nullptr;   // peer rows to unpack, grouped by source
+    uint64_t halo_send_n = 0, halo_recv_n = 0;
+    std::vector<uint64_t> halo_send_rows_off, halo_recv_rows_off;         // rows, world + 1
+    double* d_halo_send = nullptr;
+    double* d_halo_recv = nullptr;
+    uint64_t halo_rows_total = 0;      // rows this rank receives per exchange (diagnostics)
     double* d_gfull[2] = {nullptr, nullptr};
     unsigned* d_counter = nullptr;    // [0, 64): row-chunk schedulers per shard; [64, 128): heavy-row schedulers
     unsigned* d_heavy = nullptr;      // per shard: local rows of degree >= heavy_deg, by degree descending
@@ -253,11 +266,17 @@ void dfree(fc_ctx* ctx, T** p) {
 }
 
 // ---- kernel-class timing ------------------------------------------------------
+// NVTX range per phase (header-only nvtx3; free when no tool is attached): the phase
+// names show up as ranges in a timeline profiler around the kernels they enqueue.
+static const char* const kClsName[] = {"fc:step", "fc:gram", "fc:sweep", "fc:rowsum",
+                                       "fc:combine", "fc:finalize", "fc:comm"};
+
 struct ProfScope {
     fc_ctx* ctx;
     int cls;
     cudaEvent_t a = nullptr, b = nullptr;
     ProfScope(fc_ctx* c, int k) : ctx(c), cls(k) {
+        nvtxRangePushA(kClsName[k]);
         if (!ctx->profiling) return;
         if (ctx->ev_pool.size() < 2) {
             for (int i = 0; i < 64; ++i) {
@@ -271,6 +290,7 @@ struct ProfScope {
         cudaEventRecord(a, ctx->stream);
     }
     ~ProfScope() {
+        nvtxRangePop();
         if (!ctx->profiling) return;
         cudaEventRecord(b, ctx->stream);
         ctx->prof_events.push_back({cls, {a, b}});
@@ -656,6 +676,10 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
         else dfree(ctx, &ctx->d_xs[k]);
     }
     TRY(dalloc(ctx, &ctx->d_prod, L));
+    if (ctx->halo) {
+        TRY(dalloc(ctx, &ctx->d_halo_send, std::max<uint64_t>(1, ctx->halo_send_n) * c));
+        TRY(dalloc(ctx, &ctx->d_halo_recv, std::max<uint64_t>(1, ctx->halo_recv_n) * c));
+    }
     for (int k = 0; k < 3; ++k) {
         if (bt) TRY(dalloc(ctx, &ctx->d_rowterm[k], L));
         else dfree(ctx, &ctx->d_rowterm[k]);
@@ -861,8 +885,34 @@ int phase_finalize(fc_ctx* ctx, int kind, int mat_mask) {
 }
 
 // allgather of the rows of U[buf] each rank owns (NCCL contexts only)
-int phase_allgather(fc_ctx* ctx, int buf) {
+int phase_halo(fc_ctx* ctx, int buf) {
+    ProfScope p(ctx, kClsComm);
+    const uint32_t c = ctx->c;
+    const unsigned blocks = (unsigned)ctx->sm_count * 4;
+    if (ctx->halo_send_n) {
+        k_halo_pack<<<blocks, 256, 0, ctx->stream>>>(ctx->d_U[buf], ctx->d_halo_send_rows, ctx->halo_send_n, c,
+                                                      ctx->d_halo_send);
+        TRY(check_launch(ctx, "k_halo_pack"));
+    }
+    std::vector<uint64_t> so(ctx->world + 1), ro(ctx->world + 1), po(ctx->world);
+    for (int r = 0; r <= ctx->world; ++r) {
+        so[r] = ctx->halo_send_rows_off[r] * c;
+        ro[r] = ctx->halo_recv_rows_off[r] * c;
+    }
+    for (int r = 0; r < ctx->world; ++r) po[r] = ctx->halo_peer_off[r] * c;
+    XP(ctx->xport->exchange(ctx->d_halo_send, so.data(), ctx->d_halo_recv, ro.data(), po.data(), ctx->stream,
+                            &ctx->err));
+    if (ctx->halo_recv_n) {
+        k_halo_unpack<<<blocks, 256, 0, ctx->stream>>>(ctx->d_halo_recv, ctx->d_halo_recv_rows, ctx->halo_recv_n, c,
+                                                        ctx->d_U[buf]);
+        TRY(check_launch(ctx, "k_halo_unpack"));
+    }
+    return FC_OK;
+}
+
+int phase_allgather(fc_ctx* ctx, int buf, bool full = false) {
     if (!ctx->xport) return FC_OK;
+    if (ctx->halo && !full) return phase_halo(ctx, buf);
     ProfScope p(ctx, kClsComm);
     XP(ctx->xport->allgather_rows(ctx->d_U[buf], ctx->bounds.data(), ctx->c, ctx->stream, &ctx->err));
     return FC_OK;
@@ -1221,6 +1271,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
         ctx->step_wide2 = std::strcmp(sp, "wide1") != 0;
     }
     if (const char* fu = std::getenv("FC_FUSE")) ctx->fuse_gram = std::strcmp(fu, "1") == 0;
+    if (const char* ha = std::getenv("FC_HALO")) ctx->halo_mode = std::atoi(ha);
     if (const char* gr = std::getenv("FC_GRAPHS")) ctx->graphs = std::strcmp(gr, "0") != 0;
     {
         const unsigned hw = std::thread::hardware_concurrency();
@@ -1319,6 +1370,13 @@ int fc_set_parity_mode(fc_ctx* ctx, int mode) {
 
 int fc_get_parity_mode(const fc_ctx* ctx) { return ctx && ctx->tol ? 1 : 0; }
 
+int fc_halo_info(const fc_ctx* ctx, uint64_t* recv_rows, uint64_t* send_rows) {
+    if (!ctx) return set_err(nullptr, FC_INVALID, "null context");
+    if (recv_rows) *recv_rows = ctx->halo ? ctx->halo_recv_n : 0;
+    if (send_rows) *send_rows = ctx->halo ? ctx->halo_send_n : 0;
+    return ctx->halo ? 1 : 0;
+}
+
 int fc_create_virtual(fc_ctx** out, int device, int shards) {
     if (shards > 32) return set_err(nullptr, FC_INVALID, "at most 32 virtual shards");
     int rc = create_common(out, device, 0, 1, shards, nullptr);
@@ -1347,6 +1405,10 @@ void fc_destroy(fc_ctx* ctx) {
     dfree(ctx, &ctx->d_totals);
     dfree(ctx, &ctx->d_chain_in);
     dfree(ctx, &ctx->d_rows_scratch);
+    dfree(ctx, &ctx->d_halo_send_rows);
+    dfree(ctx, &ctx->d_halo_recv_rows);
+    dfree(ctx, &ctx->d_halo_send);
+    dfree(ctx, &ctx->d_halo_recv);
     dfree(ctx, &ctx->d_counter);
     dfree(ctx, &ctx->d_state);
     dfree(ctx, &ctx->d_trace);
@@ -1389,6 +1451,102 @@ int fc_plan_partition(uint64_t n, const int64_t* row_ptr, int world, uint64_t* b
         bounds[r] = std::max<uint64_t>(bounds[r - 1], std::min<uint64_t>(pick * kBlock, n));
     }
     bounds[world] = n;
+    return FC_OK;
+}
+
+// Halo plan (multi-rank, SURVEY.md 8(e) "locality graphs"): rank r's sweep gathers only
+// the U rows its shard's columns name, so it needs its own rows plus the "halo"
+// H_r = {j : j in a column of r's rows, owner(j) != r}.  Every rank holds the full CSR
+// on the host, so each computes all H_r (one bitmap per rank) and from them its send
+// lists (H_p intersected with its own range, per peer p), its receive list (H_r, grouped
+// by owner) and, for the loopback transport, where its segment sits in each peer's
+// packed send buffer.  The decision (halo vs full allgather) is taken from the complete
+// count matrix, so every rank decides the same.
+static int plan_halo(fc_ctx* ctx, uint64_t n, const int64_t* row_ptr, const uint32_t* col_idx) {
+    const int W = ctx->world, me = ctx->rank;
+    const std::vector<uint64_t>& bd = ctx->bounds;
+    const size_t words = (n + 63) / 64;
+    std::vector<std::vector<uint64_t>> bits(W, std::vector<uint64_t>(words, 0));
+    auto owner = [&](uint64_t j) {
+        return (int)(std::upper_bound(bd.begin(), bd.end(), j) - bd.begin()) - 1;
+    };
+    {
+        std::vector<std::thread> th;
+        for (int r = 0; r < W; ++r)
+            th.emplace_back([&, r] {
+                const uint64_t lo = bd[r], hi = bd[r + 1];
+                auto& B = bits[r];
+                for (uint64_t i = lo; i < hi; ++i)
+                    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+                        const uint64_t j = col_idx[e];
+                        if (j < lo || j >= hi) B[j >> 6] |= 1ULL << (j & 63);
+                    }
+            });
+        for (auto& t : th) t.join();
+    }
+    // cnt[q][r] = |H_r intersected with range(q)|
+    std::vector<std::vector<uint64_t>> cnt(W, std::vector<uint64_t>(W, 0));
+    for (int r = 0; r < W; ++r)
+        for (uint64_t w = 0; w < words; ++w) {
+            uint64_t m = bits[r][w];
+            while (m) {
+                const uint64_t j = (w << 6) + (uint64_t)__builtin_ctzll(m);
+                m &= m - 1;
+                cnt[owner(j)][r]++;
+            }
+        }
+    bool use = ctx->halo_mode == 1;
+    if (ctx->halo_mode < 0) {   // auto: every rank receives less than half of what the allgather moves
+        use = true;
+        for (int r = 0; r < W; ++r) {
+            uint64_t recv = 0;
+            for (int q = 0; q < W; ++q) recv += cnt[q][r];
+            if (2 * recv >= n - (bd[r + 1] - bd[r])) use = false;
+        }
+    }
+    ctx->halo = use;
+    if (!use) return FC_OK;
+    // receive list: H_me ascending (grouped by owner, ranges are contiguous)
+    std::vector<unsigned> recv_rows;
+    ctx->halo_recv_rows_off.assign(W + 1, 0);
+    for (uint64_t w = 0; w < words; ++w) {
+        uint64_t m = bits[me][w];
+        while (m) {
+            recv_rows.push_back((unsigned)((w << 6) + (uint64_t)__builtin_ctzll(m)));
+            m &= m - 1;
+        }
+    }
+    for (int q = 0; q < W; ++q) ctx->halo_recv_rows_off[q + 1] = ctx->halo_recv_rows_off[q] + cnt[q][me];
+    // send lists: for each destination r ascending, the own rows in H_r
+    std::vector<unsigned> send_rows;
+    ctx->halo_send_rows_off.assign(W + 1, 0);
+    for (int r = 0; r < W; ++r) {
+        if (r != me) {
+            for (uint64_t j = bd[me]; j < bd[me + 1]; ++j)
+                if ((bits[r][j >> 6] >> (j & 63)) & 1ULL) send_rows.push_back((unsigned)j);
+        }
+        ctx->halo_send_rows_off[r + 1] = send_rows.size();
+    }
+    // my segment in peer p's send buffer: rows p sends to ranks before me
+    ctx->halo_peer_off.assign(W, 0);
+    for (int p = 0; p < W; ++p) {
+        uint64_t off = 0;
+        for (int r = 0; r < me; ++r)
+            if (r != p) off += cnt[p][r];
+        ctx->halo_peer_off[p] = off;
+    }
+    ctx->halo_send_n = send_rows.size();
+    ctx->halo_recv_n = recv_rows.size();
+    ctx->halo_rows_total = recv_rows.size();
+    TRY(dalloc(ctx, &ctx->d_halo_send_rows, std::max<size_t>(1, send_rows.size())));
+    TRY(dalloc(ctx, &ctx->d_halo_recv_rows, std::max<size_t>(1, recv_rows.size())));
+    if (!send_rows.empty())
+        CU(cudaMemcpyAsync(ctx->d_halo_send_rows, send_rows.data(), send_rows.size() * sizeof(unsigned),
+                           cudaMemcpyHostToDevice, ctx->stream));
+    if (!recv_rows.empty())
+        CU(cudaMemcpyAsync(ctx->d_halo_recv_rows, recv_rows.data(), recv_rows.size() * sizeof(unsigned),
+                           cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     return FC_OK;
 }
 
@@ -1535,6 +1693,11 @@ static int upload_csr_impl(fc_ctx* ctx, uint64_t n, uint64_t nnz, const int64_t*
         }
     }
     ctx->local_nnz = lnnz;
+    ctx->halo = false;
+    if (ctx->xport && ctx->world > 1 && ctx->halo_mode != 0 && !src_device) {
+        HostPhase hp("halo plan");
+        TRY(plan_halo(ctx, n, row_ptr, col_idx));
+    }
     {   // fingerprint of the shard CSR (checked by fc_solver_resume); before hot flags are set
         HostPhase hp("fingerprint+sync");
         unsigned long long* d_fp = reinterpret_cast<unsigned long long*>(ctx->d_counter + 96);
@@ -1967,6 +2130,12 @@ int fc_solver_end(fc_ctx* ctx, double* x_out, fc_trace_record* trace, uint64_t t
         TRY(session_done(ctx, &done));
     }
     const DevState& s = *ctx->h_state;
+    // halo mode: the replicas hold only own + halo rows; complete the result first (every
+    // rank calls fc_solver_end, so this collective matches across ranks)
+    if (ctx->halo) {
+        TRY(phase_allgather(ctx, s.result_buf, true));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
     HostPhase hp("result d2h");
     if (x_out) TRY(d2h_big(ctx, x_out, ctx->d_U[s.result_buf], ctx->n * ctx->c * sizeof(double)));
     // device-held records; when the caller's buffer is smaller, its last slot gets the

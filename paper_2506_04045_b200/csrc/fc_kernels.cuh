@@ -1576,6 +1576,28 @@ __global__ void k_hvp_rows(const double* g2, const double* vs, const double* x, 
     }
 }
 
+// Halo exchange (locality graphs, multi-rank): rows of U listed in `rows` <-> a packed
+// buffer [i][C].  Lanes run over components, so each row moves as one coalesced segment.
+__global__ void k_halo_pack(const double* __restrict__ U, const unsigned* __restrict__ rows, unsigned long long n,
+                            unsigned C, double* __restrict__ out) {
+    const unsigned long long total = n * C;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long i = e / C, k = e % C;
+        out[e] = U[(size_t)rows[i] * C + k];
+    }
+}
+
+__global__ void k_halo_unpack(const double* __restrict__ in, const unsigned* __restrict__ rows, unsigned long long n,
+                              unsigned C, double* __restrict__ U) {
+    const unsigned long long total = n * C;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long i = e / C, k = e % C;
+        U[(size_t)rows[i] * C + k] = in[e];
+    }
+}
+
 // Structural check of an uploaded CSR (fc_upload_csr accepts caller arrays): row_ptr
 // monotone, column indices < n and strictly ascending within a row -- the invariants
 // from_triplets establishes (sparse.hpp:43-58) and every gathering kernel relies on.
@@ -1845,21 +1867,38 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
             const int t = (p + sub) * LD + lg;
             cp_async8(TA + t, A + a);
             if (mode != kLiteral) cp_async8(TB + t, Bp + a);
-            const size_t q = (size_t)row * C + lg;
-            if (TOL && mode != kLiteral)                     // S X_ext = S bar + beta (S bar - S bar_prev)
-                TX[t] = extrap(ldg(XS + q), ldg(sp.XSB + q), sp.beta);
-            else
-                cp_async8(TX + t, XS + q);
+            cp_async8(TX + t, XS + (size_t)row * C + lg);
         }
     }
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
+    double xr[G];
     if (row_ok) {
-        double xr[G];
 #pragma unroll
         for (int l = 0; l < G; ++l)
             xr[l] = (EXACT || l < C) ? ((mode == kLiteral) ? ra[l] : extrap(ra[l], rb_[l], sp.beta)) : 0.0;
+    }
+    if constexpr (TOL) {
+        // S X_ext = S bar + beta (S bar - S bar_prev): S bar_prev rows into the B tile,
+        // which is dead once x is in registers (a second round trip, coalesced)
+        if (mode != kLiteral) {
+            __syncwarp();
+            for (int p = 0; p < 32; p += RPW) {
+                const unsigned long long row = rb + p + sub;
+                if (row < rend && lane_ok) cp_async8(TB + (p + sub) * LD + lg, sp.XSB + (size_t)row * C + lg);
+            }
+            cp_async_commit();
+            cp_async_wait_all();
+            __syncwarp();
+            for (int p = 0; p < 32; p += RPW) {
+                const int t = (p + sub) * LD + lg;
+                if (rb + p + sub < rend && lane_ok) TX[t] = extrap(TX[t], TB[t], sp.beta);
+            }
+            __syncwarp();
+        }
+    }
+    if (row_ok) {
         double mi = 0.0;                                     // BT: <xs_i, x_i>, component order
         if constexpr (BT) {
 #pragma unroll
@@ -2573,10 +2612,8 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             const int r = e / CP, k = e % CP;
             if (k < C) {
                 const size_t q = (size_t)(rb + r) * C + k;
-                if (TOL && sp.mode != kLiteral)              // S X_ext = S bar + beta (S bar - S bar_prev)
-                    TY[r * LD + k] = extrap(ldg(sp.XS + q), ldg(sp.XSB + q), sp.beta);
-                else
-                    cp_async8(TY + r * LD + k, sp.XS + q);
+                cp_async8(TY + r * LD + k, sp.XS + q);
+                if (TOL && sp.mode != kLiteral) cp_async8(CS + r * LD + k, sp.XSB + q);   // S bar_prev
             }
         }
         cp_async_commit();
@@ -2621,7 +2658,10 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             for (int j = 0; j < KT; ++j) {
                 const int k = KT * kg + j;
                 if (r < rows && k < C) {
-                    const double grad = dmul(-4.0, dsub(TY[r * LD + k], o[i][j]));
+                    double xsv = TY[r * LD + k];
+                    if (TOL && sp.mode != kLiteral)          // S X_ext = S bar + beta (S bar - S bar_prev)
+                        xsv = extrap(xsv, CS[r * LD + k], sp.beta);
+                    const double grad = dmul(-4.0, dsub(xsv, o[i][j]));
                     TY[r * LD + k] = dsub(TX[r * LD + k], dmul(sp.tau, grad));
                 }
             }

@@ -38,6 +38,12 @@ struct Transport {
     virtual int recv_prev(double* dst, size_t n, cudaStream_t s, std::string* err) = 0;
     virtual int send_next(const double* src, size_t n, cudaStream_t s, std::string* err) = 0;
     virtual int bcast_last(double* buf, size_t n, cudaStream_t s, std::string* err) = 0;
+    // halo exchange (locality graphs): send[send_off[p] .. send_off[p+1]) to every peer p,
+    // recv[recv_off[p] .. recv_off[p+1]) from every peer p (offsets in doubles, world + 1
+    // entries each).  peer_off[p]: where this rank's segment starts in p's send buffer
+    // (used by the loopback, which pulls; NCCL matches send/recv pairs itself).
+    virtual int exchange(const double* send, const uint64_t* send_off, double* recv, const uint64_t* recv_off,
+                         const uint64_t* peer_off, cudaStream_t s, std::string* err) = 0;
 };
 
 inline int transport_fail(std::string* err, const char* what, const char* detail) {
@@ -76,13 +82,26 @@ struct NcclTransport final : Transport {
     int bcast_last(double* buf, size_t n, cudaStream_t s, std::string* err) override {
         return chk(ncclBroadcast(buf, buf, n, ncclDouble, world - 1, comm, s), err, "ncclBroadcast");
     }
+    int exchange(const double* send, const uint64_t* send_off, double* recv, const uint64_t* recv_off,
+                 const uint64_t*, cudaStream_t s, std::string* err) override {
+        if (int e = chk(ncclGroupStart(), err, "ncclGroupStart")) return e;
+        for (int p = 0; p < world; ++p) {
+            if (p == rank) continue;
+            const size_t ns = send_off[p + 1] - send_off[p], nr = recv_off[p + 1] - recv_off[p];
+            if (ns)
+                if (int e = chk(ncclSend(send + send_off[p], ns, ncclDouble, p, comm, s), err, "ncclSend")) return e;
+            if (nr)
+                if (int e = chk(ncclRecv(recv + recv_off[p], nr, ncclDouble, p, comm, s), err, "ncclRecv")) return e;
+        }
+        return chk(ncclGroupEnd(), err, "ncclGroupEnd");
+    }
 };
 
 }  // namespace fc
 
 // ---- in-process loopback group (shared by the W rank contexts) ---------------------------
 struct fc_loopback {
-    enum Kind { kAllgather = 0, kChain = 1, kBcast = 2, kKinds = 3 };
+    enum Kind { kAllgather = 0, kChain = 1, kBcast = 2, kHalo = 3, kKinds = 4 };
     static constexpr int kRing = 8;
     struct Slot {
         uint64_t seq = ~0ULL;          // publication held in this slot
@@ -142,7 +161,7 @@ namespace fc {
 struct LoopbackTransport final : Transport {
     fc_loopback* g;
     int rank, world;
-    uint64_t ag_seq = 0, send_seq = 0, recv_seq = 0, bc_seq = 0;
+    uint64_t ag_seq = 0, send_seq = 0, recv_seq = 0, bc_seq = 0, halo_seq = 0;
     LoopbackTransport(fc_loopback* grp, int r) : g(grp), rank(r), world(grp->world) {}
     const char* name() const override { return "loopback"; }
     int allgather_rows(double* buf, const uint64_t* bounds, uint32_t c, cudaStream_t s, std::string* err) override {
@@ -168,6 +187,24 @@ struct LoopbackTransport final : Transport {
     int send_next(const double* src, size_t n, cudaStream_t s, std::string* err) override {
         (void)n;
         return g->publish(fc_loopback::kChain, rank, send_seq++, src, s, 1, err);
+    }
+    int exchange(const double* send, const uint64_t* send_off, double* recv, const uint64_t* recv_off,
+                 const uint64_t* peer_off, cudaStream_t s, std::string* err) override {
+        const uint64_t seq = halo_seq++;
+        int consumers = 0;
+        for (int p = 0; p < world; ++p) consumers += (p != rank && send_off[p + 1] > send_off[p]);
+        if (consumers)
+            if (int e = g->publish(fc_loopback::kHalo, rank, seq, send, s, consumers, err)) return e;
+        for (int p = 0; p < world; ++p) {
+            const size_t nr = recv_off[p + 1] - recv_off[p];
+            if (p == rank || !nr) continue;
+            if (int e = g->consume(fc_loopback::kHalo, p, seq, s, err, [&](const void* ptr) {
+                    return cudaMemcpyAsync(recv + recv_off[p], static_cast<const double*>(ptr) + peer_off[p],
+                                           nr * sizeof(double), cudaMemcpyDeviceToDevice, s);
+                }))
+                return e;
+        }
+        return 0;
     }
     int bcast_last(double* buf, size_t n, cudaStream_t s, std::string* err) override {
         const uint64_t seq = bc_seq++;

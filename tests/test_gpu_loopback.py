@@ -95,3 +95,70 @@ def test_loopback_empty_shards(oracle, world):
     assert int(res[0][0][1]) - int(res[0][0][0]) in (0, 1024, 1500)
     for _, got in res:
         same(got, want)
+
+
+# ---- halo exchange (locality graphs): only the rows other shards reference move ------------
+def run_ranks_env(world, g, x0, conf, env):
+    import os
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    group = capi.LoopbackGroup(world)
+    out, errs = [None] * world, []
+
+    def rank(r):
+        try:
+            ctx = group.context(r)
+            try:
+                ctx.upload(g)
+                out[r] = (ctx.halo_info(), ctx.solve(x0, conf))
+            finally:
+                ctx.close()
+        except Exception as e:
+            errs.append((r, repr(e)))
+
+    try:
+        th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+    finally:
+        group.close()
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("method", [GPA, FISTA])
+def test_halo_exchange_locality_graph_bitwise(oracle, world, method):
+    """Citation graph in time order (locality=1): neighbours are near in id space, the
+    automatic plan picks the halo exchange, and every rank's result equals the oracle."""
+    import paper_2506_04045_b200 as fc
+    g = fc.generate_citation(60_000, 600_000, seed=3, locality=True)
+    x0 = oracle.init_random(g.n, 16, 5)
+    kw = dict(method=method, max_iter=6, fista_restart=True)
+    want = oracle.solve(g, x0, **kw)
+    res = run_ranks_env(world, g, x0, capi.Context.config(**kw), {})
+    for (mode, recv, _), got in res:
+        assert mode == 1 and recv < g.n // 2
+        same(got, want)
+
+
+def test_halo_exchange_forced_on_random_graph(oracle):
+    g = random_graph(12_000, 7.0, 77)
+    x0 = oracle.init_random(g.n, 8, 6)
+    kw = dict(method=FISTA, max_iter=5, fista_restart=True, step_size=40 * oracle.default_step_size(g))
+    want = oracle.solve(g, x0, **kw)
+    res = run_ranks_env(3, g, x0, capi.Context.config(**kw), {"FC_HALO": "1"})
+    for (mode, _, _), got in res:
+        assert mode == 1
+        same(got, want)
+    res = run_ranks_env(3, g, x0, capi.Context.config(**kw), {"FC_HALO": "0"})
+    for (mode, _, _), got in res:
+        assert mode == 0
+        same(got, want)
