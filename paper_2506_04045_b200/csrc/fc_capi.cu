@@ -100,7 +100,8 @@ struct fc_ctx {
     cudaStream_t side = nullptr;       // Gram next to the sweep (independent within an iteration)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool overlap = false;              // FC_OVERLAP=1: Gram on a side stream (measured: no gain)
-    int overlap2 = 0;                  // FC_OVERLAP=2[:k]: persistent Gram (k CTAs per SM) launched before the sweep
+    int overlap2 = 1;                  // persistent Gram (k CTAs per SM) launched before the sweep on a side
+                                       // stream (default k = 1; FC_OVERLAP=0 disables, =2:k sets k)
     fc::Transport* xport = nullptr;    // multi-rank collectives (NCCL or in-process loopback); null = one rank
     int sm_count = 148;
     std::string err;
@@ -1284,7 +1285,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
     CU(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     if (const char* ov = std::getenv("FC_OVERLAP")) {
         ctx->overlap = std::strcmp(ov, "1") == 0;
-        if (ov[0] == '2') ctx->overlap2 = ov[1] == ':' ? std::max(1, std::atoi(ov + 2)) : 1;
+        ctx->overlap2 = ov[0] == '2' ? (ov[1] == ':' ? std::max(1, std::atoi(ov + 2)) : 1) : 0;
     }
     CU(cudaMalloc(&ctx->d_state, sizeof(DevState)));
     CU(cudaMallocHost(&ctx->h_state, sizeof(DevState)));

@@ -1794,6 +1794,30 @@ constexpr int kStepThreads = 128;
 #define FC_STEP_KU 4
 #endif
 
+// Tolerance mode's projection threshold (Michelot 1986): theta = (sum_S y - 1) / |S| with
+// S = {y > theta}, starting from S = all entries; theta only grows and S only shrinks, so
+// the loop stops when a pass drops nothing (typically 2-4 passes over the row).  Equals the
+// sorted-prefix threshold of simplex.hpp:29-36 in exact arithmetic.
+__device__ __forceinline__ double michelot_threshold(const double* y, int C) {
+    double sum = 0.0;
+    for (int k = 0; k < C; ++k) sum += y[k];
+    int cnt = C;
+    double thr = (sum - 1.0) / (double)cnt;
+    for (int it = 0; it < C; ++it) {
+        double s2 = 0.0;
+        int c2 = 0;
+        for (int k = 0; k < C; ++k)
+            if (y[k] > thr) {
+                s2 += y[k];
+                ++c2;
+            }
+        if (c2 == cnt || c2 == 0) break;
+        cnt = c2;
+        thr = (s2 - 1.0) / (double)cnt;
+    }
+    return thr;
+}
+
 // Per-kernel invariants of a k_step_t / k_step_gram batch (read from the plan once).
 struct StepPlan {
     const double* A;                                         // bar^{n-1} (or the literal point)
@@ -1940,6 +1964,14 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
             bad = true;
         } else if (C == 1) {
             tr[0] = 1.0;
+        } else if constexpr (TOL) {
+            // tolerance mode: sort-free Michelot projection (same threshold in exact
+            // arithmetic, any summation order; no residual folds -- they move the top
+            // entries by rounding-size amounts only)
+            const double thr = michelot_threshold(tr, C);
+#pragma unroll
+            for (int k = 0; k < G; ++k)
+                if (EXACT || k < C) tr[k] = ref_max(tr[k] - thr, 0.0);
         } else {
             const double thr = row_threshold<G>(tr, C);
             double w[G];
@@ -2528,8 +2560,8 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
 // K3 for 32 < C <= 128 (no backtracking terms), v2: G resident in shared memory
 // for the whole launch, batches of 32 rows per CTA of 256 threads:
 //   1 X_ext rows -> TX (formed in registers, solver.hpp:261), S X_ext -> TY (cp.async)
-//   2 gradient as a register-tiled GEMM: thread (row group of 4 = its warp, k group
-//     of KT = CP/32 adjacent components) accumulates o[r][k] = sum_{l ascending}
+//   2 gradient as a register-tiled GEMM: thread (row group of 4 = its warp, KT = CP/32
+//     components k = 64p + 2kg + {0,1}) accumulates o[r][k] = sum_{l ascending}
 //     G[k][l] x_r[l] -- each output one sequential DMUL+DADD chain, the reference's
 //     order (objective.hpp:37-43); no barrier inside the l loop
 //   3 y = x - tau (-4 (xs - o)) in place of xs (objective.hpp:116-117, solver.hpp:102)
@@ -2625,22 +2657,19 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             for (int j = 0; j < KT; ++j) o[i][j] = 0.0;
         {
             const double* xrow = TX + (4 * rg) * LD;
-            const double* gcol = GS + KT * kg;
+            // lane kg owns components k = 64 p + 2 kg + {0, 1} (p < KT/2): each double2 load of
+            // a G row is then 16 consecutive bytes per lane, conflict-free across the warp
+            const double* gcol = GS + 2 * kg;
 #pragma unroll 4
             for (int l = 0; l < CP; ++l) {
                 double xv[4], gv[KT];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) xv[i] = xrow[i * LD + l];
-                if constexpr (KT % 2 == 0) {
 #pragma unroll
-                    for (int j = 0; j < KT; j += 2) {
-                        const double2 t = *reinterpret_cast<const double2*>(gcol + l * CP + j);
-                        gv[j] = t.x;
-                        gv[j + 1] = t.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < KT; ++j) gv[j] = gcol[l * CP + j];
+                for (int j = 0; j < KT; j += 2) {
+                    const double2 t = *reinterpret_cast<const double2*>(gcol + l * CP + 32 * j);
+                    gv[j] = t.x;
+                    gv[j + 1] = t.y;
                 }
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -2656,7 +2685,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             const int r = 4 * rg + i;
 #pragma unroll
             for (int j = 0; j < KT; ++j) {
-                const int k = KT * kg + j;
+                const int k = 32 * (j & ~1) + 2 * kg + (j & 1);   // the GEMM's component map
                 if (r < rows && k < C) {
                     double xsv = TY[r * LD + k];
                     if (TOL && sp.mode != kLiteral)          // S X_ext = S bar + beta (S bar - S bar_prev)
@@ -2682,6 +2711,46 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
         const bool row_fin = __all_sync(gmask, fin);
         if (live && !row_fin) bad = true;
         const bool work = live && row_fin && C > 1;
+        double* yrow = TY + pr * LD;
+        if constexpr (TOL) {
+            // tolerance mode: sort-free Michelot threshold over the 8 lanes' slots
+            // (michelot_threshold's iteration; partial sums reduced across the lanes)
+            if (work) {
+                double sum = 0.0;
+#pragma unroll
+                for (int m = 0; m < VPL; ++m)
+                    if (VPL * pq + m < C) sum += v[m];
+#pragma unroll
+                for (int o2 = 1; o2 < 8; o2 <<= 1) sum += __shfl_xor_sync(gmask, sum, o2);
+                int cnt = C;
+                double thr = (sum - 1.0) / (double)cnt;
+                for (int it = 0; it < C; ++it) {
+                    double s2 = 0.0;
+                    int c2 = 0;
+#pragma unroll
+                    for (int m = 0; m < VPL; ++m)
+                        if (VPL * pq + m < C && v[m] > thr) {
+                            s2 += v[m];
+                            ++c2;
+                        }
+#pragma unroll
+                    for (int o2 = 1; o2 < 8; o2 <<= 1) {
+                        s2 += __shfl_xor_sync(gmask, s2, o2);
+                        c2 += __shfl_xor_sync(gmask, c2, o2);
+                    }
+                    if (c2 == cnt || c2 == 0) break;
+                    cnt = c2;
+                    thr = (s2 - 1.0) / (double)cnt;
+                }
+#pragma unroll
+                for (int m = 0; m < VPL; ++m) {
+                    const int k = VPL * pq + m;
+                    if (k < C) yrow[k] = ref_max(v[m] - thr, 0.0);
+                }
+            } else if (live && row_fin && C == 1 && pq == 0) {
+                yrow[0] = 1.0;
+            }
+        } else {
 #pragma unroll
         for (int kk = 2; kk <= CP; kk <<= 1) {
 #pragma unroll
@@ -2714,7 +2783,6 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
         }
         double* srow = TX + pr * LD;                         // sorted values
         double* crow = CS + pr * LD;                         // their running sums
-        double* yrow = TY + pr * LD;
 #pragma unroll
         for (int m = 0; m < VPL; ++m) srow[VPL * pq + m] = v[m];
         __syncwarp();
@@ -2781,6 +2849,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
                     if (yrow[k] == top) yrow[k] = ref_max(dsub(yrow[k], share), 0.0);
             }
             __syncwarp();
+        }
         }
         __syncthreads();
         // 5: store bar^n

@@ -136,10 +136,11 @@ def run_ranks_env(world, g, x0, conf, env):
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("method", [GPA, FISTA])
 def test_halo_exchange_locality_graph_bitwise(oracle, world, method):
-    """Citation graph in time order (locality=1): neighbours are near in id space, the
-    automatic plan picks the halo exchange, and every rank's result equals the oracle."""
+    """Block model with contiguous blocks (locality=1): 90% of the edges stay inside a
+    block, so a shard references few rows of the others; the automatic plan picks the
+    halo exchange, and every rank's result equals the oracle."""
     import paper_2506_04045_b200 as fc
-    g = fc.generate_citation(60_000, 600_000, seed=3, locality=True)
+    g = fc.generate_sbm(64_000, 128_000, 16, seed=3, p_in=0.97, locality=True)
     x0 = oracle.init_random(g.n, 16, 5)
     kw = dict(method=method, max_iter=6, fista_restart=True)
     want = oracle.solve(g, x0, **kw)
