@@ -45,7 +45,9 @@ def main():
         t_ref = time.perf_counter() - t1
         rec_ok = [r[:3] for r in ours["records"]] == [tuple(r[:3]) for r in want["records"]]
         res = {
-            "config": name, "n": g.n, "nnz": g.nnz, "k": cfg["c"], "method": cfg["method"], "iterations": k,
+            # the reference has no backtracking: config B (bench method fista_bt) compares plain FISTA
+            "config": name, "n": g.n, "nnz": g.nnz, "k": cfg["c"], "method": "gpa" if method == GPA else "fista",
+            "iterations": k,
             "x0_identical": same_x0,
             "records_identical": rec_ok,
             "reason_iterations_identical": (ours["reason"], ours["iterations"]) == (want["reason"], want["iterations"]),
