@@ -779,23 +779,27 @@ int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr, unsigned max
     const bool few = ctx->local_blocks < (uint64_t)ctx->sm_count * 2;
     // 8x8 tiles from C = 64 (fewer shared loads per FP64 pair, and one CTA covers all
     // tiles of a block instead of re-staging its rows for several tile groups)
+    // tile shape TR x TC; FC_GRAM_TS = 1 | 4 | 8 (square) | 48 (4 x 8)
     int TS = few ? 1 : (c >= 64 ? 8 : 4);
     if (const char* e = std::getenv("FC_GRAM_TS")) {
         const int v = std::atoi(e);
-        if (v == 1 || v == 4 || v == 8) TS = v;
+        if (v == 1 || v == 4 || v == 8 || v == 48) TS = v;
     }
-    const int nT = ((int)c + TS - 1) / TS;
-    const int tiles = nT * (nT + 1) / 2 * (dual ? 2 : 1);
+    const int TR = TS == 48 ? 4 : TS, TC = TS == 48 ? 8 : TS;
+    const int tiles = gram_tiles((int)c, TR, TC) * (dual ? 2 : 1);
     int R = gram_rows_per_chunk(c);
     if (few) R = std::max(R, std::min(128, 4096 / (int)((c + 3) & ~3u)));
-    if (TS == 8) R = std::max(8, std::min(16, 2048 / (int)((c + 7) & ~7u)));
+    if (TC == 8) R = std::max(8, std::min(16, 2048 / (int)((c + 7) & ~7u)));
     if (const char* e = std::getenv("FC_GRAM_R")) R = std::max(1, std::min(128, std::atoi(e)));
-    const size_t smem = gram_smem((int)c, dual ? 1 : 0, R, TS);
-    static PerDevice<size_t[18]> smem_set_pd;
-    size_t (&smem_set)[18] = smem_set_pd(ctx);
-    auto kfn = ctx->tol ? (TS == 1 ? k_gram<1, true> : (TS == 8 ? k_gram<8, true> : k_gram<4, true>))
-                        : (TS == 1 ? k_gram<1> : (TS == 8 ? k_gram<8> : k_gram<4>));
-    const int sidx = TS + (ctx->tol ? 9 : 0);
+    const size_t smem = gram_smem((int)c, dual ? 1 : 0, R, std::max(TR, TC));
+    static PerDevice<size_t[128]> smem_set_pd;
+    size_t (&smem_set)[128] = smem_set_pd(ctx);
+    auto pick = [&](auto tol) {
+        constexpr bool T = decltype(tol)::value;
+        return TS == 1 ? k_gram<1, 1, T> : TS == 8 ? k_gram<8, 8, T> : TS == 48 ? k_gram<4, 8, T> : k_gram<4, 4, T>;
+    };
+    auto kfn = ctx->tol ? pick(std::true_type{}) : pick(std::false_type{});
+    const int sidx = (TS % 64) + (ctx->tol ? 64 : 0);
     if (smem > 48 * 1024 && smem > smem_set[sidx]) {
         CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         smem_set[sidx] = smem;
@@ -928,49 +932,47 @@ int enqueue_prelude(fc_ctx* ctx) {   // FISTA loss at x0 (solver.hpp:206-212)
     return FC_OK;
 }
 
-// Gram and sweep of one iteration both only read the new iterate.  Opt-in
-// (FC_OVERLAP=1): the Gram on a side stream next to the sweep, launched after it so
-// the heavy rows start at once.  Measured no gain (the persistent sweep holds the
-// register file until its tail), so the default is sequential.
-static int gram_and_sweep(fc_ctx* ctx) {
+// After the step: the exchange of the new rows, the Gram partials of the new iterate (and of
+// the next extrapolated point) and the sweep.  The Gram reads only this rank's rows, so by
+// default (FC_OVERLAP unset or 2[:k]) it runs as a persistent grid (k CTAs per SM) on a side
+// stream, launched first: concurrent with the row exchange (NCCL / loopback copies) and with
+// the HBM-bound sweep, whose memory stalls its FP64 work fills.  FC_OVERLAP=1: the round-1
+// variant (Gram launched after the sweep); FC_OVERLAP=0: sequential.
+static int exchange_gram_sweep(fc_ctx* ctx, int buf, bool dual_sweep) {
     if (ctx->overlap2 && !ctx->profiling) {
-        // persistent Gram grid (one CTA per SM) launched FIRST on the side stream, then the
-        // sweep: the FP64-bound Gram runs in the memory stalls of the HBM-bound sweep
         CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
         CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
         TRY(phase_gram(ctx, true, ctx->side, (unsigned)ctx->sm_count * ctx->overlap2));
-        TRY(phase_sweep(ctx, true));
+        TRY(phase_allgather(ctx, buf));
+        TRY(phase_sweep(ctx, dual_sweep));
         CU(cudaEventRecord(ctx->join_ev, ctx->side));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
         return FC_OK;
     }
+    TRY(phase_allgather(ctx, buf));
     if (ctx->overlap && !ctx->xport && !ctx->profiling) {
         CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
         CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
-        TRY(phase_sweep(ctx, true));
+        TRY(phase_sweep(ctx, dual_sweep));
         TRY(phase_gram(ctx, true, ctx->side));
         CU(cudaEventRecord(ctx->join_ev, ctx->side));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
         return FC_OK;
     }
     TRY(phase_gram(ctx, true));
-    return phase_sweep(ctx, true);
+    return phase_sweep(ctx, dual_sweep);
 }
 
 int enqueue_fista_iteration(fc_ctx* ctx, int bt) {
-    if (ctx->tol) {                                  // single gather: S X_ext by linearity in the next step
-        TRY(phase_step(ctx, 0));
-        TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
-        TRY(phase_gram(ctx, true));
-        TRY(phase_sweep(ctx, false));
-    } else if (fused_step_gram(ctx, bt)) {
+    const int buf = ctx->ag_buf >= 0 ? ctx->ag_buf : (int)(ctx->host_iter % 3);
+    if (!ctx->tol && fused_step_gram(ctx, bt)) {
         TRY(phase_step_gram(ctx));
-        TRY(phase_allgather(ctx, (int)(ctx->host_iter % 3)));
+        TRY(phase_allgather(ctx, buf));
         TRY(phase_sweep(ctx, true));
     } else {
-        TRY(phase_step(ctx, bt));
-        TRY(phase_allgather(ctx, ctx->ag_buf >= 0 ? ctx->ag_buf : (int)(ctx->host_iter % 3)));
-        TRY(gram_and_sweep(ctx));
+        // tolerance mode: single-gather sweep (S X_ext by linearity in the next step)
+        TRY(phase_step(ctx, ctx->tol ? 0 : bt));
+        TRY(exchange_gram_sweep(ctx, buf, !ctx->tol));
     }
     TRY(phase_rowsum(ctx, bt));
     TRY(phase_combine(ctx, 3, bt ? 0xF : 1));

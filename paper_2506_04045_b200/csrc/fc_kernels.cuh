@@ -975,6 +975,14 @@ __global__ void __launch_bounds__(kRowsumThreads) k_rowsum(Bufs b, Geo g, int ns
 // =============================================================================
 constexpr int kGramMaxThreads = 320;   // blockDim = min(320, tiles rounded up to a warp)
 
+// Number of TR x TC tiles of one C x C Gram that hold at least one pair r <= s.
+__host__ __device__ inline int gram_tiles(int C, int TR, int TC) {
+    const int nR = (C + TR - 1) / TR, nC = (C + TC - 1) / TC;
+    int t = 0;
+    for (int J = 0; J < nC; ++J) t += min(nR - 1, (TC * J + TC - 1) / TR) + 1;
+    return t;
+}
+
 // Shared memory of k_gram: 2 stages x (bar [+ prev]) x R x C4, + the ext tile (dual).
 __host__ __device__ inline size_t gram_smem(int C, int dual, int R, int TS = 4) {
     const int PADW = TS > 4 ? TS : 4;
@@ -985,24 +993,31 @@ __host__ __device__ inline size_t gram_smem(int C, int dual, int R, int TS = 4) 
 // TS x TS register tiles: TS = 4 in general; TS = 1 when there are few 1024-row
 // blocks (small N): every (r, s) pair gets its own thread, so the 1024-long
 // sequential chains of all pairs run in parallel instead of 16 per thread.
-template <int TS, bool TOL = false>
+template <int TR, int TC = TR, bool TOL = false>
 __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dual, int rows_per_chunk) {
     const DevState* st = b.st;
     if (st->done) return;
     extern __shared__ double smg[];
     const int C = (int)g.C;
-    constexpr int PADW = TS > 4 ? TS : 4;
+    constexpr int PADW = (TR > TC ? TR : TC) > 4 ? (TR > TC ? TR : TC) : 4;
     const int C4 = (C + PADW - 1) / PADW * PADW;         // row stride in shared memory
-    const int nT = (C + TS - 1) / TS;
-    const int tiles_per_mat = nT * (nT + 1) / 2;
+    const int nR = (C + TR - 1) / TR, nC = (C + TC - 1) / TC;
+    // tiles (I, J) of TR x TC that hold at least one pair r <= s: I <= (TC J + TC - 1) / TR
+    const int tiles_per_mat = gram_tiles(C, TR, TC);
     const int nmat = dual ? 2 : 1;
     const int tile = blockIdx.y * blockDim.x + threadIdx.x;
     const bool has = tile < tiles_per_mat * nmat;
     const int mat_local = has ? tile / tiles_per_mat : 0;
     int tt = has ? tile % tiles_per_mat : 0;
-    int I = 0;
-    while (tt >= nT - I) { tt -= nT - I; ++I; }
-    const int J = I + tt;
+    int I = 0, J = 0;
+    for (; J < nC; ++J) {
+        const int cnt = min(nR - 1, (TC * J + TC - 1) / TR) + 1;
+        if (tt < cnt) {
+            I = tt;
+            break;
+        }
+        tt -= cnt;
+    }
     // dual: local matrix 0 -> bar (slot kMatBar), 1 -> ext (slot kMatExt)
     const int out_mat = dual ? (mat_local == 0 ? kMatBar : kMatExt) : kMatExt;
 
@@ -1034,11 +1049,11 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
         cp_async_commit();
     };
 
-    double acc[TS][TS];
+    double acc[TR][TC];
 #pragma unroll
-    for (int a = 0; a < TS; ++a)
+    for (int a = 0; a < TR; ++a)
 #pragma unroll
-        for (int c = 0; c < TS; ++c) acc[a][c] = 0.0;
+        for (int c = 0; c < TC; ++c) acc[a][c] = 0.0;
 
     issue(0, r0);
     int sidx = 0;
@@ -1060,34 +1075,31 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
         if (has) {
             const double* t = mat_local == 0 ? tb : te;
             for (int rr = 0; rr < rows; ++rr) {
-                double xr[TS], xq[TS];
-                if constexpr (TS == 8) {
+                double xr[TR], xq[TC];
+                if constexpr (TR % 2 == 0 && TC % 2 == 0) {   // 16-byte aligned (C4 % 4 == 0)
                     const double2* rowp = reinterpret_cast<const double2*>(t + rr * C4);
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) {
-                        const double2 rv = rowp[4 * I + a], qv = rowp[4 * J + a];
+                    for (int a = 0; a < TR / 2; ++a) {
+                        const double2 rv = rowp[(TR / 2) * I + a];
                         xr[2 * a] = rv.x;
                         xr[2 * a + 1] = rv.y;
+                    }
+#pragma unroll
+                    for (int a = 0; a < TC / 2; ++a) {
+                        const double2 qv = rowp[(TC / 2) * J + a];
                         xq[2 * a] = qv.x;
                         xq[2 * a + 1] = qv.y;
                     }
-                } else if constexpr (TS == 4) {
-                    const double2* rowp = reinterpret_cast<const double2*>(t + rr * C4);
-                    const double2 r01 = rowp[2 * I], r23 = rowp[2 * I + 1];
-                    const double2 q01 = rowp[2 * J], q23 = rowp[2 * J + 1];
-                    xr[0] = r01.x; xr[1] = r01.y; xr[2] = r23.x; xr[3] = r23.y;
-                    xq[0] = q01.x; xq[1] = q01.y; xq[2] = q23.x; xq[3] = q23.y;
                 } else {
 #pragma unroll
-                    for (int a = 0; a < TS; ++a) {
-                        xr[a] = t[rr * C4 + TS * I + a];
-                        xq[a] = t[rr * C4 + TS * J + a];
-                    }
+                    for (int a = 0; a < TR; ++a) xr[a] = t[rr * C4 + TR * I + a];
+#pragma unroll
+                    for (int a = 0; a < TC; ++a) xq[a] = t[rr * C4 + TC * J + a];
                 }
 #pragma unroll
-                for (int a = 0; a < TS; ++a)
+                for (int a = 0; a < TR; ++a)
 #pragma unroll
-                    for (int c = 0; c < TS; ++c) acc[a][c] = madd<TOL>(acc[a][c], xr[a], xq[c]);
+                    for (int c = 0; c < TC; ++c) acc[a][c] = madd<TOL>(acc[a][c], xr[a], xq[c]);
             }
         }
         __syncthreads();                                     // stage sidx is re-filled next round
@@ -1095,10 +1107,10 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
     if (has) {
         double* out = b.gpart[out_mat] + (size_t)blk * g.npairs;
 #pragma unroll
-        for (int a = 0; a < TS; ++a)
+        for (int a = 0; a < TR; ++a)
 #pragma unroll
-            for (int c = 0; c < TS; ++c) {
-                const int r = TS * I + a, s = TS * J + c;
+            for (int c = 0; c < TC; ++c) {
+                const int r = TR * I + a, s = TC * J + c;
                 if (r <= s && s < C) out[pair_index(r, s, C)] = acc[a][c];
             }
     }
