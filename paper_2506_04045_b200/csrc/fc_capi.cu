@@ -174,6 +174,8 @@ struct fc_ctx {
     bool step_big = false;             // FC_STEP=big: thread-per-row k_step_big for C > 32
     bool fuse_gram = false;            // FC_FUSE=1: fused k_step_gram for C <= 32 FISTA (measured slower: 8.5 vs 8.2 ms at C)
     bool tol = false;                  // fc_set_parity_mode(1): tolerance mode (FMA, single-gather FISTA)
+    bool pair_sweep = true;            // FC_PAIR=0: C <= 8 dual sweep gathers bar and prev rows separately
+    double* d_pair = nullptr;          // C <= 8: interleaved [bar | prev] rows, N x 2C
     bool step_wide2 = true;            // FC_STEP=wide1: the round-1 k_step_wide (G streamed) for 32 < C <= 128
     bool umaps_ok = false;
     UMaps umaps;                       // tensor maps of U[0..2] (TMA gather4)
@@ -388,6 +390,18 @@ int launch_sweep_small(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     return FC_OK;
 }
 
+template <int G, bool W>
+int launch_sweep_small_pair(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
+    if (!grid) grid = grid_for((const void*)k_sweep_small_pair<G, W>, 256, 0, ctx->sm_count);
+    k_sweep_small_pair<G, W><<<grid, 256, 0, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_sweep_small_pair launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
 template <int G, int S>
 struct LaunchSweep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, bool dual) {
@@ -395,6 +409,8 @@ struct LaunchSweep {
         if constexpr (G <= 8) {   // measured: C=8 9.5 vs 12.2 ms (E8); C=16 keeps the group sweep (B: 1.52 vs 1.78 ms)
             if (!ctx->sweep_groups) {
                 const bool w = ctx->weighted;
+                if (dual && b.pair)
+                    return w ? launch_sweep_small_pair<G, true>(ctx, b, g) : launch_sweep_small_pair<G, false>(ctx, b, g);
                 if (dual) return w ? launch_sweep_small<G, true, true>(ctx, b, g) : launch_sweep_small<G, true, false>(ctx, b, g);
                 return w ? launch_sweep_small<G, false, true>(ctx, b, g) : launch_sweep_small<G, false, false>(ctx, b, g);
             }
@@ -677,6 +693,8 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
         else dfree(ctx, &ctx->d_xs[k]);
     }
     TRY(dalloc(ctx, &ctx->d_prod, L));
+    if (ctx->pair_sweep && c <= 8) TRY(dalloc(ctx, &ctx->d_pair, N * 2 * c));
+    else dfree(ctx, &ctx->d_pair);
     if (ctx->halo) {
         TRY(dalloc(ctx, &ctx->d_halo_send, std::max<uint64_t>(1, ctx->halo_send_n) * c));
         TRY(dalloc(ctx, &ctx->d_halo_recv, std::max<uint64_t>(1, ctx->halo_recv_n) * c));
@@ -719,6 +737,7 @@ Bufs make_bufs(fc_ctx* ctx, size_t s) {
     b.st = ctx->d_state;
     b.counter = ctx->d_counter + s;
     b.hcounter = ctx->d_counter + 64 + s;
+    b.pair = ctx->d_pair;
     b.heavy = ctx->d_heavy ? ctx->d_heavy + ctx->heavy_off[s] : nullptr;
     b.nheavy = ctx->d_heavy ? (unsigned)ctx->heavy_cnt[s] : 0u;
     b.heavy_deg = ctx->heavy_deg;
@@ -932,6 +951,16 @@ int enqueue_prelude(fc_ctx* ctx) {   // FISTA loss at x0 (solver.hpp:206-212)
     return FC_OK;
 }
 
+// C <= 8 dual sweep: interleave the (exchanged) bar^n and bar^{n-1} rows for the PAIR gather.
+int phase_pair_pack(fc_ctx* ctx) {
+    if (!ctx->d_pair) return FC_OK;
+    ProfScope p(ctx, kClsSweep);
+    const Bufs b = make_bufs(ctx, 0);
+    const Geo g = make_geo(ctx, 0);
+    k_pair_pack<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(b, g);
+    return check_launch(ctx, "k_pair_pack");
+}
+
 // After the step: the exchange of the new rows, the Gram partials of the new iterate (and of
 // the next extrapolated point) and the sweep.  The Gram reads only this rank's rows, so by
 // default (FC_OVERLAP unset or 2[:k]) it runs as a persistent grid (k CTAs per SM) on a side
@@ -944,12 +973,14 @@ static int exchange_gram_sweep(fc_ctx* ctx, int buf, bool dual_sweep) {
         CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
         TRY(phase_gram(ctx, true, ctx->side, (unsigned)ctx->sm_count * ctx->overlap2));
         TRY(phase_allgather(ctx, buf));
+        if (dual_sweep) TRY(phase_pair_pack(ctx));
         TRY(phase_sweep(ctx, dual_sweep));
         CU(cudaEventRecord(ctx->join_ev, ctx->side));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
         return FC_OK;
     }
     TRY(phase_allgather(ctx, buf));
+    if (dual_sweep) TRY(phase_pair_pack(ctx));
     if (ctx->overlap && !ctx->xport && !ctx->profiling) {
         CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
         CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
@@ -968,6 +999,7 @@ int enqueue_fista_iteration(fc_ctx* ctx, int bt) {
     if (!ctx->tol && fused_step_gram(ctx, bt)) {
         TRY(phase_step_gram(ctx));
         TRY(phase_allgather(ctx, buf));
+        TRY(phase_pair_pack(ctx));
         TRY(phase_sweep(ctx, true));
     } else {
         // tolerance mode: single-gather sweep (S X_ext by linearity in the next step)
@@ -1275,6 +1307,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
     }
     if (const char* fu = std::getenv("FC_FUSE")) ctx->fuse_gram = std::strcmp(fu, "1") == 0;
     if (const char* ha = std::getenv("FC_HALO")) ctx->halo_mode = std::atoi(ha);
+    if (const char* pa = std::getenv("FC_PAIR")) ctx->pair_sweep = std::strcmp(pa, "0") != 0;
     if (const char* gr = std::getenv("FC_GRAPHS")) ctx->graphs = std::strcmp(gr, "0") != 0;
     {
         const unsigned hw = std::thread::hardware_concurrency();
@@ -1408,6 +1441,7 @@ void fc_destroy(fc_ctx* ctx) {
     dfree(ctx, &ctx->d_totals);
     dfree(ctx, &ctx->d_chain_in);
     dfree(ctx, &ctx->d_rows_scratch);
+    dfree(ctx, &ctx->d_pair);
     dfree(ctx, &ctx->d_halo_send_rows);
     dfree(ctx, &ctx->d_halo_recv_rows);
     dfree(ctx, &ctx->d_halo_send);

@@ -114,6 +114,7 @@ struct Bufs {
     unsigned nheavy;
     unsigned heavy_deg;
     unsigned* hcounter;             // scheduler of the heavy rows
+    double* pair;                   // C <= 8 dual sweep: rows [bar^n | bar^{n-1}] interleaved (2C doubles)
 };
 
 struct Geo {
@@ -799,10 +800,11 @@ __global__ void __launch_bounds__(kSwTmaThreads) k_sweep_tma(Bufs b, Geo g, cons
 // A warp owns a 32-row chunk and walks its rows in order; column indices of the
 // next 32 nonzeros are prefetched.
 // =============================================================================
-template <int G, bool DUAL, bool W>
-__global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
+template <int G, bool DUAL, bool W, bool PAIR>
+__device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
     const DevState* st = b.st;
     if (st->done) return;
+
     const unsigned kChunk = g.chunk;                        // rows per counter grab (<= 32)
     constexpr int Q = 32 / G;                 // nonzeros per load instruction
     constexpr int U = (32 / Q) < 8 ? (32 / Q) : 8;  // loads per lane in flight per batch (x2 DUAL)
@@ -859,6 +861,42 @@ __global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
                     nxt = __ldg(b.col + pn + lane);
                     if (W) nxtw = ldg(b.val + pn + lane);
                 }
+                if constexpr (PAIR) {
+                    // 2G lanes per neighbour: lane cp < G reads bar component cp, lane G + cp the
+                    // prev component cp of the same interleaved row; bar lanes pull prev by shuffle
+                    constexpr int GP = 2 * G, QP = 32 / GP, UP = U;
+                    const unsigned qp = lane / GP, cp = lane % GP;
+                    const bool okp = (cp % G) < C;
+                    const unsigned poff = cp < (unsigned)G ? cp : C + (cp - G);
+                    for (int t0 = 0; t0 < cnt; t0 += QP * UP) {
+                        double vb[UP], ve[UP];
+#pragma unroll
+                        for (int u = 0; u < UP; ++u) {
+                            const int k = t0 + u * QP + (int)qp;
+                            const unsigned raw = __shfl_sync(kFull, myidx, k & 31);
+                            const double w = W ? __shfl_sync(kFull, myw, k & 31) : 1.0;
+                            const bool ok = k < cnt && okp;
+                            const double v = ok ? ldg(b.pair + (size_t)(raw & kIdxMask) * (2 * C) + poff) : 0.0;
+                            const double pv = __shfl_down_sync(kFull, v, G);
+                            const double ev = extrap(v, pv, beta);
+                            ve[u] = W ? dmul(w, ev) : ev;
+                            vb[u] = W ? dmul(w, v) : v;
+                        }
+#pragma unroll
+                        for (int u = 0; u < UP; ++u) {
+#pragma unroll
+                            for (int qq = 0; qq < QP; ++qq) {
+                                const int k = t0 + u * QP + qq;
+                                const double bb = __shfl_sync(kFull, vb[u], qq * GP + c);
+                                const double ee = __shfl_sync(kFull, ve[u], qq * GP + c);
+                                if (k < cnt) {
+                                    ab = dadd(ab, bb);
+                                    ae = dadd(ae, ee);
+                                }
+                            }
+                        }
+                    }
+                } else
                 for (int t0 = 0; t0 < cnt; t0 += Q * U) {
                     double vb[U], ve[DUAL ? U : 1];
 #pragma unroll
@@ -928,6 +966,36 @@ __global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
             tdeg = heavy_deg;
         }
         strip(rb, nrow, tdeg);
+    }
+}
+
+template <int G, bool DUAL, bool W>
+__global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
+    k_sweep_small_body<G, DUAL, W, false>(b, g);
+}
+
+// PAIR (dual, C <= 8): the neighbours' bar and prev rows are read as ONE interleaved row
+// [bar | prev] of 2C doubles from b.pair (k_pair_pack): 2G lanes per neighbour, one
+// 8C..16C-byte contiguous segment per neighbour instead of two half-size ones -- a
+// random-gather microbenchmark at E8 size measured 3.15 vs 5.76 ms
+// (scripts/gather_ceiling_c8_pair.cu).  Same values, same summation order.
+template <int G, bool W>
+__global__ void __launch_bounds__(256, 4) k_sweep_small_pair(Bufs b, Geo g) {
+    k_sweep_small_body<G, true, W, true>(b, g);
+}
+
+// Interleave [bar^n | bar^{n-1}] rows for the PAIR sweep (after the row exchange).
+__global__ void k_pair_pack(Bufs b, Geo g) {
+    const DevState* st = b.st;
+    if (st->done) return;
+    const unsigned C = g.C;
+    const double* __restrict__ B = b.U[st->sw_b];
+    const double* __restrict__ P = b.U[st->sw_p];
+    const unsigned long long total = g.N * 2ull * C;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long i = e / (2 * C), k = e % (2 * C);
+        b.pair[e] = k < C ? B[i * C + k] : P[i * C + k - C];
     }
 }
 
