@@ -896,7 +896,7 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
                             }
                         }
                     }
-                } else
+                } else {
                 for (int t0 = 0; t0 < cnt; t0 += Q * U) {
                     double vb[U], ve[DUAL ? U : 1];
 #pragma unroll
@@ -927,6 +927,7 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
                             }
                         }
                     }
+                }
                 }
             }
             e = e1;
