@@ -109,7 +109,7 @@ SIGNATURES = {
     "fc_free": (None, [C.c_void_p]),
 }
 
-KERNEL_CLASSES = ("step", "gram", "sweep", "rowsum", "combine", "finalize", "comm")
+KERNEL_CLASSES = ("step", "gram", "sweep", "rowsum", "combine", "finalize", "comm", "pack")
 
 _lib = None
 

@@ -74,7 +74,7 @@ struct Shard {
     uint64_t lblk = 0, nblk = 0;       // local block offset / count
 };
 
-enum { kClsStep, kClsGram, kClsSweep, kClsRowsum, kClsCombine, kClsFinalize, kClsComm, kNumCls };
+enum { kClsStep, kClsGram, kClsSweep, kClsRowsum, kClsCombine, kClsFinalize, kClsComm, kClsPack, kNumCls };
 
 struct CopyPool {
     std::vector<std::thread> th;
@@ -174,7 +174,8 @@ struct fc_ctx {
     bool step_big = false;             // FC_STEP=big: thread-per-row k_step_big for C > 32
     bool fuse_gram = false;            // FC_FUSE=1: fused k_step_gram for C <= 32 FISTA (measured slower: 8.5 vs 8.2 ms at C)
     bool tol = false;                  // fc_set_parity_mode(1): tolerance mode (FMA, single-gather FISTA)
-    bool pair_sweep = true;            // FC_PAIR=0: C <= 8 dual sweep gathers bar and prev rows separately
+    bool pair_sweep = false;           // FC_PAIR=1: C <= 8 dual sweep gathers interleaved [bar | prev] rows
+                                       // (measured E8: 6.34 incl. pack vs 6.41 ms -- within noise, off)
     double* d_pair = nullptr;          // C <= 8: interleaved [bar | prev] rows, N x 2C
     bool step_wide2 = true;            // FC_STEP=wide1: the round-1 k_step_wide (G streamed) for 32 < C <= 128
     bool umaps_ok = false;
@@ -272,7 +273,7 @@ void dfree(fc_ctx* ctx, T** p) {
 // NVTX range per phase (header-only nvtx3; free when no tool is attached): the phase
 // names show up as ranges in a timeline profiler around the kernels they enqueue.
 static const char* const kClsName[] = {"fc:step", "fc:gram", "fc:sweep", "fc:rowsum",
-                                       "fc:combine", "fc:finalize", "fc:comm"};
+                                       "fc:combine", "fc:finalize", "fc:comm", "fc:pack"};
 
 struct ProfScope {
     fc_ctx* ctx;
@@ -954,7 +955,7 @@ int enqueue_prelude(fc_ctx* ctx) {   // FISTA loss at x0 (solver.hpp:206-212)
 // C <= 8 dual sweep: interleave the (exchanged) bar^n and bar^{n-1} rows for the PAIR gather.
 int phase_pair_pack(fc_ctx* ctx) {
     if (!ctx->d_pair) return FC_OK;
-    ProfScope p(ctx, kClsSweep);
+    ProfScope p(ctx, kClsPack);
     const Bufs b = make_bufs(ctx, 0);
     const Geo g = make_geo(ctx, 0);
     k_pair_pack<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(b, g);
@@ -1307,7 +1308,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
     }
     if (const char* fu = std::getenv("FC_FUSE")) ctx->fuse_gram = std::strcmp(fu, "1") == 0;
     if (const char* ha = std::getenv("FC_HALO")) ctx->halo_mode = std::atoi(ha);
-    if (const char* pa = std::getenv("FC_PAIR")) ctx->pair_sweep = std::strcmp(pa, "0") != 0;
+    if (const char* pa = std::getenv("FC_PAIR")) ctx->pair_sweep = std::strcmp(pa, "1") == 0;
     if (const char* gr = std::getenv("FC_GRAPHS")) ctx->graphs = std::strcmp(gr, "0") != 0;
     {
         const unsigned hw = std::thread::hardware_concurrency();

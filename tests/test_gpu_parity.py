@@ -449,3 +449,23 @@ def test_upload_rejects_malformed_csr():
         t.solve(x0, cfg(method=GPA, max_iter=2))
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("c", [1, 3, 5, 8])
+@pytest.mark.parametrize("vshards", [1, 3])
+def test_pair_layout_sweep_bitwise(oracle, monkeypatch, c, vshards):
+    """FC_PAIR=1 (opt-in): the C <= 8 dual sweep gathers interleaved [bar | prev] rows
+    (k_pair_pack + k_sweep_small_pair); FISTA with restart and with backtracking stay
+    bitwise equal to the oracle (heavy rows included: FC_HEAVY_DEG=16)."""
+    monkeypatch.setenv("FC_PAIR", "1")
+    monkeypatch.setenv("FC_HEAVY_DEG", "16")
+    g = random_graph(9000, 12.0, 60 + c)
+    x0 = oracle.init_random(g.n, c, 2)
+    t = capi.Context(0) if vshards == 1 else capi.Context(0, virtual_shards=vshards)
+    try:
+        t.upload(g)
+        for kw in (dict(method=FISTA, max_iter=8, fista_restart=True, step_size=40 * oracle.default_step_size(g)),
+                   dict(method=FISTA_BT, max_iter=5, step_size=300 * oracle.default_step_size(g))):
+            assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+    finally:
+        t.close()
