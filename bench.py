@@ -501,6 +501,35 @@ def main():
     except Exception:
         pass
 
+    # FP64-issue rooflines of the step and Gram kernels (secondary: not the dominant kernel).
+    # Under the bitwise contract every DADD / DMUL is one FP64 lane-op (no FMA), so the
+    # ceiling is 64 FP64 lanes per SM x SMs x the SM clock.  Algorithmic ops per row:
+    #   step: gradient 2C^2 + extrapolation 3C + grad/step 4C;  Gram (dual): 2 C(C+1) + 3C.
+    secondary = None
+    if kt is not None and prof_iters:
+        try:
+            props = torch.cuda.get_device_properties(local)
+            sms = props.multi_processor_count
+        except Exception:
+            sms = 148
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                clk_max = float(json.load(f).get("sm_max_mhz", 1965.0))
+        except Exception:
+            clk_max = 1965.0
+        fp64_peak = 64 * sms * clk_max * 1e6 / 1e12          # Tops/s of DADD / DMUL
+        rows_l = hi - lo
+        cc = cfg["c"]
+        secondary = {}
+        for name, ops_row in (("step", 2 * cc * cc + 7 * cc), ("gram", 2 * cc * (cc + 1) + 3 * cc)):
+            ms_k = kt[name][0] / prof_iters if name in kt else 0.0
+            if ms_k > 0:
+                ach = ops_row * rows_l / (ms_k / 1e3) / 1e12
+                secondary[name] = {"bound": "fp64 issue (no-FMA bitwise contract)", "achieved": ach, "peak": fp64_peak,
+                                   "unit": "Tops/s", "frac": ach / fp64_peak, "ops_per_row": ops_row,
+                                   "ms_per_step": ms_k,
+                                   "peak_source": f"64 FP64 lanes/SM x {sms} SMs x {clk_max:.0f} MHz"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import reference_available
@@ -560,6 +589,7 @@ def main():
                          "kernel": "k_sweep", "algorithmic_bytes_per_launch": sweep_b,
                          "avg_launch_ms": sweep_avg, "peak_source": peak_kind},
             "kernel_ms_per_step": ({k: v[0] / prof_iters for k, v in kt.items()} if prof_iters else None),
+            "secondary_rooflines": secondary,
             "kernel_timing": "per-kernel CUDA events on the library stream, second pass of the same K iterations",
             "gpu_launches": launches,
             "e2e": e2e,

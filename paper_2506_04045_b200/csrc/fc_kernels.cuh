@@ -2741,9 +2741,9 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             // lane kg owns components k = 64 p + 2 kg + {0, 1} (p < KT/2): each double2 load of
             // a G row is then 16 consecutive bytes per lane, conflict-free across the warp
             const double* gcol = GS + 2 * kg;
-#pragma unroll 4
-            for (int l = 0; l < CP; ++l) {
-                double xv[4], gv[KT];
+            // register double buffer: the operands of l + 1 are loaded while l is multiplied
+            double xa[4], ga[KT], xb[4], gb[KT];
+            auto load = [&](double (&xv)[4], double (&gv)[KT], int l) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) xv[i] = xrow[i * LD + l];
 #pragma unroll
@@ -2752,10 +2752,20 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
                     gv[j] = t.x;
                     gv[j + 1] = t.y;
                 }
+            };
+            auto fma_step = [&](const double (&xv)[4], const double (&gv)[KT]) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < KT; ++j) o[i][j] = madd<TOL>(o[i][j], gv[j], xv[i]);
+            };
+            load(xa, ga, 0);
+#pragma unroll 2
+            for (int l = 0; l < CP; l += 2) {
+                load(xb, gb, l + 1);
+                fma_step(xa, ga);
+                if (l + 2 < CP) load(xa, ga, l + 2);
+                fma_step(xb, gb);
             }
         }
         // 3: grad and step, in place of xs
