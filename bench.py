@@ -82,8 +82,15 @@ def shared_graph(cfg, name, rank, world):
     /dev/shm; every rank maps that file (zero-copy, one page-cache copy for the node)
     instead of each rank regenerating the whole graph in host memory."""
     import paper_2506_04045_b200 as fc
-    path = os.path.join("/dev/shm" if os.path.isdir("/dev/shm") else "/tmp",
-                        f"fc_bench_{name}_{cfg['n']}_{cfg['m']}_{GRAPH_SEED}.fccsr")
+    need = 8 * (cfg["n"] + 1) + 4 * (2 * cfg["m"] + cfg["n"]) + (1 << 26)   # upper bound of the file
+    root = "/tmp"
+    try:
+        st = os.statvfs("/dev/shm")
+        if st.f_bavail * st.f_frsize > 2 * need:          # a container's /dev/shm may be tiny
+            root = "/dev/shm"
+    except OSError:
+        pass
+    path = os.path.join(root, f"fc_bench_{name}_{cfg['n']}_{cfg['m']}_{GRAPH_SEED}.fccsr")
     if rank == 0 and not os.path.exists(path):
         g = make_graph(cfg)
         tmp = path + f".{os.getpid()}.tmp"
