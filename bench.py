@@ -91,6 +91,11 @@ def shared_graph(cfg, name, rank, world):
     except OSError:
         pass
     path = os.path.join(root, f"fc_bench_{name}_{cfg['n']}_{cfg['m']}_{GRAPH_SEED}.fccsr")
+    if world > 1:                                          # rank 0's choice of directory for everyone
+        import torch.distributed as dist
+        obj = [path]
+        dist.broadcast_object_list(obj, src=0)
+        path = obj[0]
     if rank == 0 and not os.path.exists(path):
         g = make_graph(cfg)
         tmp = path + f".{os.getpid()}.tmp"
