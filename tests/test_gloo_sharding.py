@@ -130,3 +130,48 @@ def test_two_rank_schedule_is_bitwise_single_process(n, c):
     want = O.solve(g, x0, method=GPA, max_iter=iters)
     assert out[0][0] == [r[1] for r in want["records"]]
     assert np.frombuffer(out[0][1], dtype=np.float64).reshape(n, c).tobytes() == want["membership"].tobytes()
+
+
+def _graph_worker(rank, world, port, q):
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import hashlib
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import bench
+        cfg = dict(bench.CONFIGS["A"])
+        cfg["m"] = 50_000 + port % 97          # a file name no earlier run left behind
+        g = bench.shared_graph(cfg, "Atest", rank, world)
+        h = hashlib.sha256(np.asarray(g.row_ptr).tobytes() + np.asarray(g.col_idx).tobytes()).hexdigest()
+        dist.barrier()
+        q.put((rank, h, g.n, g.nnz))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e), 0, 0))
+
+
+def test_bench_shared_graph_world2():
+    """bench.py N > 1: rank 0 writes the graph once (FCCSR001), every rank maps the same
+    bytes -- and they equal a direct generation."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_graph_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert out[0][1] == out[1][1] and len(out[0][1]) == 64, out
+    sys.path.insert(0, ROOT)
+    import hashlib
+    import bench
+    cfg = dict(bench.CONFIGS["A"])
+    cfg["m"] = 50_000 + port % 97
+    g = bench.make_graph(cfg)
+    assert hashlib.sha256(g.row_ptr.tobytes() + g.col_idx.tobytes()).hexdigest() == out[0][1]
+    import glob
+    for f in glob.glob("/dev/shm/fc_bench_Atest_*") + glob.glob("/tmp/fc_bench_Atest_*"):
+        os.remove(f)
