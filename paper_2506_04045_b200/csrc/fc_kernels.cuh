@@ -2654,16 +2654,22 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
 // Padding: G is zero outside C x C and x is zero beyond C, so the padded GEMM terms
 // add +0 to chains that start at +0 and can never be -0: exact.
 // =============================================================================
-constexpr int kW2Threads = 256;
-constexpr int kW2Rows = 32;
+constexpr int kW2Threads = 256;                             // two independent groups of 128
+constexpr int kW2Group = 128;
+constexpr int kW2Rows = 16;                                 // rows per group batch
 
 template <int CP>
 struct Wide2Cfg {
     static constexpr int LD = CP + 1;
     static constexpr int KT = CP / 32;                      // k per thread in the GEMM
     static constexpr int VPL = CP / 8;                      // values per lane in the projection
-    static size_t smem() { return sizeof(double) * ((size_t)CP * CP + (size_t)3 * kW2Rows * LD); }
+    static size_t smem() { return sizeof(double) * ((size_t)CP * CP + (size_t)2 * 3 * kW2Rows * LD); }
 };
+
+// barrier of one 128-thread group (ids 1, 2; 0 is __syncthreads)
+__device__ __forceinline__ void group_sync(int grp) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kW2Group) : "memory");
+}
 
 template <int CP, bool TOL = false>
 __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
@@ -2674,32 +2680,36 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
     constexpr int VPL = Wide2Cfg<CP>::VPL;
     constexpr int R = kW2Rows;
     extern __shared__ double smw2[];
+    // two groups of 128 threads share G and work on separate 16-row batches with their own
+    // tiles and barriers, so one group's FP64 GEMM overlaps the other's projection
+    const int grp = threadIdx.x / kW2Group;
+    const int tid = threadIdx.x % kW2Group;
     double* GS = smw2;                                       // GS[l*CP + k] = G[k][l]
-    double* TX = GS + CP * CP;
+    double* TX = GS + CP * CP + (size_t)grp * 3 * R * LD;
     double* TY = TX + R * LD;
     double* CS = TY + R * LD;                                // running sums of the sorted rows
     const int C = (int)g.C;
-    const int tid = threadIdx.x;
     const StepPlan sp = step_plan(b);
     {
         const double* __restrict__ Gt = b.gfull[st->step_sel];   // Gt[l*C + k] == G[k][l]
-        for (int e = tid; e < CP * CP; e += kW2Threads) {
+        for (int e = threadIdx.x; e < CP * CP; e += kW2Group) {
             const int l = e / CP, k = e % CP;
             GS[e] = (l < C && k < C) ? Gt[l * C + k] : 0.0;
         }
     }
-    const int rg = tid >> 5, kg = tid & 31;                  // GEMM: rows 4rg..4rg+3, k = KT*kg + j
+    __syncthreads();
+    const int rg = tid >> 5, kg = tid & 31;                  // GEMM: rows 4rg..4rg+3 (rg < 4), k map below
     const int pr = tid >> 3, pq = tid & 7;                   // projection: row pr, lane pq of 8
     const unsigned gmask = 0xFFu << ((tid & 31) & ~7);
     bool bad = false;
-    for (unsigned long long rb = (unsigned long long)blockIdx.x * R; rb < g.nrows;
-         rb += (unsigned long long)gridDim.x * R) {
+    for (unsigned long long rb = ((unsigned long long)blockIdx.x * 2 + grp) * R; rb < g.nrows;
+         rb += (unsigned long long)gridDim.x * 2 * R) {
         const int rows = (int)min((unsigned long long)R, g.nrows - rb);
-        __syncthreads();                                     // previous batch's tiles consumed (and GS staged)
+        group_sync(grp);                                     // previous batch's tiles consumed
         // 1: A -> TX, B -> TY (cp.async), X_ext formed in place in TX (solver.hpp:261), then
         //    S X_ext -> TY, which lands while the GEMM runs (it is read only after it)
 #pragma unroll 4
-        for (int e = tid; e < R * CP; e += kW2Threads) {
+        for (int e = tid; e < R * CP; e += kW2Group) {
             const int r = e / CP, k = e % CP;
             if (r < rows && k < C) {
                 const size_t a = (size_t)(g.row0 + rb + r) * C + k;
@@ -2711,17 +2721,17 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
         }
         cp_async_commit();
         cp_async_wait_all();
-        __syncthreads();
+        group_sync(grp);
         if (sp.mode != kLiteral) {
 #pragma unroll 4
-            for (int e = tid; e < rows * CP; e += kW2Threads) {
+            for (int e = tid; e < rows * CP; e += kW2Group) {
                 const int r = e / CP, k = e % CP;
                 if (k < C) TX[r * LD + k] = extrap(TX[r * LD + k], TY[r * LD + k], sp.beta);
             }
-            __syncthreads();
+            group_sync(grp);
         }
 #pragma unroll 4
-        for (int e = tid; e < rows * CP; e += kW2Threads) {
+        for (int e = tid; e < rows * CP; e += kW2Group) {
             const int r = e / CP, k = e % CP;
             if (k < C) {
                 const size_t q = (size_t)(rb + r) * C + k;
@@ -2770,7 +2780,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
         }
         // 3: grad and step, in place of xs
         cp_async_wait_all();
-        __syncthreads();
+        group_sync(grp);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int r = 4 * rg + i;
@@ -2786,7 +2796,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
                 }
             }
         }
-        __syncthreads();
+        group_sync(grp);
         // 4: projection, warp-local: warp w owns rows 4w..4w+3, 8 lanes per row
         // 4a: finiteness, register bitonic sort (descending) -> TX (x is dead)
         const bool live = pr < rows;
@@ -2942,9 +2952,9 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             __syncwarp();
         }
         }
-        __syncthreads();
+        group_sync(grp);
         // 5: store bar^n
-        for (int e = tid; e < rows * CP; e += kW2Threads) {
+        for (int e = tid; e < rows * CP; e += kW2Group) {
             const int r = e / CP, k = e % CP;
             if (k < C) sp.D[(size_t)(g.row0 + rb + r) * C + k] = TY[r * LD + k];
         }
