@@ -478,7 +478,7 @@ int launch_step_wide2(fc_ctx* ctx, const Bufs& b, const Geo& g) {
         CU(cudaFuncSetAttribute(k_step_wide2<CP, TOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         grid = grid_for((const void*)k_step_wide2<CP, TOL>, kW2Threads, smem, ctx->sm_count);
     }
-    const unsigned long long need = (g.nrows + kW2Rows - 1) / kW2Rows;
+    const unsigned long long need = (g.nrows + Wide2Cfg<CP>::R - 1) / Wide2Cfg<CP>::R;
     const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
     k_step_wide2<CP, TOL><<<gr, kW2Threads, smem, ctx->stream>>>(b, g);
     ctx->launches++;

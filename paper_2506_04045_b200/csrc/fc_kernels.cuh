@@ -2654,21 +2654,25 @@ __global__ void __launch_bounds__(kWideThreads) k_step_wide(Bufs b, Geo g) {
 // Padding: G is zero outside C x C and x is zero beyond C, so the padded GEMM terms
 // add +0 to chains that start at +0 and can never be -0: exact.
 // =============================================================================
-constexpr int kW2Threads = 256;                             // two independent groups of 128
-constexpr int kW2Group = 128;
-constexpr int kW2Rows = 16;                                 // rows per group batch
+constexpr int kW2Threads = 256;                             // NG = 256 / GT independent groups
 
 template <int CP>
 struct Wide2Cfg {
     static constexpr int LD = CP + 1;
     static constexpr int KT = CP / 32;                      // k per thread in the GEMM
     static constexpr int VPL = CP / 8;                      // values per lane in the projection
-    static size_t smem() { return sizeof(double) * ((size_t)CP * CP + (size_t)2 * 3 * kW2Rows * LD); }
+    // threads per group (measured: CP = 128 -> 128 threads: E128 step 26.2 vs 30.2 ms with 64;
+    // CP = 64 -> 64 threads: E64 step 11.2 vs 11.9 ms with 128)
+    static constexpr int GT = CP == 64 ? 64 : 128;
+    static constexpr int NG = kW2Threads / GT;
+    static constexpr int R = GT / 8;                        // rows per group batch (8 lanes per row)
+    static size_t smem() { return sizeof(double) * ((size_t)CP * CP + (size_t)NG * 3 * R * LD); }
 };
 
-// barrier of one 128-thread group (ids 1, 2; 0 is __syncthreads)
+// barrier of one group (ids 1..NG; 0 is __syncthreads)
+template <int GT>
 __device__ __forceinline__ void group_sync(int grp) {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kW2Group) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(GT) : "memory");
 }
 
 template <int CP, bool TOL = false>
@@ -2678,7 +2682,8 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
     constexpr int LD = Wide2Cfg<CP>::LD;
     constexpr int KT = Wide2Cfg<CP>::KT;
     constexpr int VPL = Wide2Cfg<CP>::VPL;
-    constexpr int R = kW2Rows;
+    constexpr int R = Wide2Cfg<CP>::R;
+    constexpr int kW2Group = Wide2Cfg<CP>::GT;
     extern __shared__ double smw2[];
     // two groups of 128 threads share G and work on separate 16-row batches with their own
     // tiles and barriers, so one group's FP64 GEMM overlaps the other's projection
@@ -2686,13 +2691,14 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
     const int tid = threadIdx.x % kW2Group;
     double* GS = smw2;                                       // GS[l*CP + k] = G[k][l]
     double* TX = GS + CP * CP + (size_t)grp * 3 * R * LD;
+    constexpr int NG = Wide2Cfg<CP>::NG;
     double* TY = TX + R * LD;
     double* CS = TY + R * LD;                                // running sums of the sorted rows
     const int C = (int)g.C;
     const StepPlan sp = step_plan(b);
     {
         const double* __restrict__ Gt = b.gfull[st->step_sel];   // Gt[l*C + k] == G[k][l]
-        for (int e = threadIdx.x; e < CP * CP; e += kW2Group) {
+        for (int e = threadIdx.x; e < CP * CP; e += kW2Threads) {
             const int l = e / CP, k = e % CP;
             GS[e] = (l < C && k < C) ? Gt[l * C + k] : 0.0;
         }
@@ -2702,10 +2708,10 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
     const int pr = tid >> 3, pq = tid & 7;                   // projection: row pr, lane pq of 8
     const unsigned gmask = 0xFFu << ((tid & 31) & ~7);
     bool bad = false;
-    for (unsigned long long rb = ((unsigned long long)blockIdx.x * 2 + grp) * R; rb < g.nrows;
-         rb += (unsigned long long)gridDim.x * 2 * R) {
+    for (unsigned long long rb = ((unsigned long long)blockIdx.x * NG + grp) * R; rb < g.nrows;
+         rb += (unsigned long long)gridDim.x * NG * R) {
         const int rows = (int)min((unsigned long long)R, g.nrows - rb);
-        group_sync(grp);                                     // previous batch's tiles consumed
+        group_sync<kW2Group>(grp);                                     // previous batch's tiles consumed
         // 1: A -> TX, B -> TY (cp.async), X_ext formed in place in TX (solver.hpp:261), then
         //    S X_ext -> TY, which lands while the GEMM runs (it is read only after it)
 #pragma unroll 4
@@ -2721,14 +2727,14 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
         }
         cp_async_commit();
         cp_async_wait_all();
-        group_sync(grp);
+        group_sync<kW2Group>(grp);
         if (sp.mode != kLiteral) {
 #pragma unroll 4
             for (int e = tid; e < rows * CP; e += kW2Group) {
                 const int r = e / CP, k = e % CP;
                 if (k < C) TX[r * LD + k] = extrap(TX[r * LD + k], TY[r * LD + k], sp.beta);
             }
-            group_sync(grp);
+            group_sync<kW2Group>(grp);
         }
 #pragma unroll 4
         for (int e = tid; e < rows * CP; e += kW2Group) {
@@ -2780,7 +2786,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
         }
         // 3: grad and step, in place of xs
         cp_async_wait_all();
-        group_sync(grp);
+        group_sync<kW2Group>(grp);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int r = 4 * rg + i;
@@ -2796,7 +2802,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
                 }
             }
         }
-        group_sync(grp);
+        group_sync<kW2Group>(grp);
         // 4: projection, warp-local: warp w owns rows 4w..4w+3, 8 lanes per row
         // 4a: finiteness, register bitonic sort (descending) -> TX (x is dead)
         const bool live = pr < rows;
@@ -2952,7 +2958,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
             __syncwarp();
         }
         }
-        group_sync(grp);
+        group_sync<kW2Group>(grp);
         // 5: store bar^n
         for (int e = tid; e < rows * CP; e += kW2Group) {
             const int r = e / CP, k = e % CP;
