@@ -58,6 +58,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+DEBUG_LIB = os.path.join(LIBDIR, "libfuzzyclust_cuda_debug.so")
+
+
+def build_debug(force: bool = False) -> str:
+    """The same library with device-side bounds checks on every gathered / scattered row
+    index (-DFC_DEBUG_CHECKS: FC_DCHECK in fc_kernels.cuh traps with the location).  Used
+    by tests/test_gpu_debug_checks.py in place of compute-sanitizer, which the GPU pool
+    does not allow."""
+    if not force and os.path.exists(DEBUG_LIB) and all(os.path.getmtime(p) <= os.path.getmtime(DEBUG_LIB)
+                                                       for p in DEPS):
+        return DEBUG_LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    tmp = DEBUG_LIB + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, "-DFC_DEBUG_CHECKS", "-I" + os.path.join(ROOT, "include"), "-o", tmp, *SOURCES,
+           "-lnccl"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, DEBUG_LIB)
+    return DEBUG_LIB
+
+
 DROPIN_SRC = os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp")
 DROPIN_BIN = os.path.join(ROOT, "tests", "cpp", "_build", "dropin_test")
 

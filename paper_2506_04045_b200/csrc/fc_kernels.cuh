@@ -171,6 +171,24 @@ __device__ __forceinline__ double ldg_hint(const double* p, unsigned long long p
 constexpr unsigned kHotBit = 0x80000000u;
 constexpr unsigned kIdxMask = 0x7fffffffu;
 
+// Device-side bounds checks of the debug build (-DFC_DEBUG_CHECKS,
+// lib/libfuzzyclust_cuda_debug.so; compute-sanitizer is not available on the GPU pool):
+// every gathered / scattered row index is checked against its array before use; a failed
+// check prints the location and traps (the context reports a device error).
+#ifdef FC_DEBUG_CHECKS
+#define FC_DCHECK(cond)                                                                    \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("FC_DCHECK failed: %s at %s:%d\n", #cond, __FILE__, __LINE__);          \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define FC_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -386,7 +404,7 @@ template <int G, int S, bool DUAL, bool W, bool EXACT>
 __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const double* __restrict__ P, double beta,
                                             unsigned myidx, double myw, int cnt, unsigned gmask, unsigned lg,
                                             unsigned C, double (&ab)[S], double (&ae)[S], unsigned long long pol_hot,
-                                            unsigned long long pol_cold) {
+                                            unsigned long long pol_cold, unsigned long long N) {
     constexpr int U = SweepTune<G, S>::U;
     if (cnt == G) {
 #pragma unroll
@@ -398,6 +416,7 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
                 const unsigned raw = __shfl_sync(gmask, myidx, k0 + u, G);
                 const unsigned o = (raw & kIdxMask) * C;
                 const unsigned long long pol = (raw & kHotBit) ? pol_hot : pol_cold;
+                FC_DCHECK((raw & kIdxMask) < N);
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const bool okc = EXACT || lg + s * G < C;
@@ -428,6 +447,7 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
                 const unsigned o = (raw & kIdxMask) * C;
                 const unsigned long long pol = (raw & kHotBit) ? pol_hot : pol_cold;
                 const bool ok = k0 + u < cnt;
+                FC_DCHECK(!ok || (raw & kIdxMask) < N);
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const bool okc = ok && (EXACT || lg + s * G < C);
@@ -529,7 +549,7 @@ __global__ void __launch_bounds__(256, SweepTune<G, S>::MINB) k_sweep(Bufs b, Ge
                     nxt_idx = __ldg(b.col + pn + lg);
                     if (W) nxt_w = ldg(b.val + pn + lg);
                 }
-                sweep_chunk<G, S, DUAL, W, EXACT>(B, P, beta, myidx, myw, cnt, gmask, lg, C, ab, ae, pol_hot, pol_cold);
+                sweep_chunk<G, S, DUAL, W, EXACT>(B, P, beta, myidx, myw, cnt, gmask, lg, C, ab, ae, pol_hot, pol_cold, g.N);
             }
             e = e1;
             double a[S];
@@ -876,6 +896,7 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
                             const unsigned raw = __shfl_sync(kFull, myidx, k & 31);
                             const double w = W ? __shfl_sync(kFull, myw, k & 31) : 1.0;
                             const bool ok = k < cnt && okp;
+                            FC_DCHECK(!ok || (raw & kIdxMask) < g.N);
                             const double v = ok ? ldg(b.pair + (size_t)(raw & kIdxMask) * (2 * C) + poff) : 0.0;
                             const double pv = __shfl_down_sync(kFull, v, G);
                             const double ev = extrap(v, pv, beta);
@@ -906,6 +927,7 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
                         const double w = W ? __shfl_sync(kFull, myw, k & 31) : 1.0;
                         const bool ok = k < cnt && okc;
                         const unsigned o = (raw & kIdxMask) * C;
+                        FC_DCHECK(!ok || (raw & kIdxMask) < g.N);
                         double bv = ok ? ldg(B + o) : 0.0;
                         if (DUAL) {
                             const double pv = ok ? ldg(P + o) : 0.0;
@@ -1665,6 +1687,7 @@ __global__ void k_halo_pack(const double* __restrict__ U, const unsigned* __rest
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
          e += (unsigned long long)gridDim.x * blockDim.x) {
         const unsigned long long i = e / C, k = e % C;
+        FC_DCHECK(rows[i] < 0x80000000u);
         out[e] = U[(size_t)rows[i] * C + k];
     }
 }
@@ -2083,6 +2106,7 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
 #pragma unroll 4
     for (int p = 0; p < 32; p += RPW) {
         const unsigned long long r2 = rb + p + sub;
+        FC_DCHECK(r2 >= rend || g.row0 + r2 < g.N);
         if (r2 < rend && lane_ok) sp.D[(size_t)(g.row0 + r2) * C + lg] = TX[(p + sub) * LD + lg];
     }
     __syncwarp();
@@ -2962,6 +2986,7 @@ __global__ void __launch_bounds__(kW2Threads, 1) k_step_wide2(Bufs b, Geo g) {
         // 5: store bar^n
         for (int e = tid; e < rows * CP; e += kW2Group) {
             const int r = e / CP, k = e % CP;
+            FC_DCHECK(g.row0 + rb + r < g.N);
             if (k < C) sp.D[(size_t)(g.row0 + rb + r) * C + k] = TY[r * LD + k];
         }
     }
