@@ -174,6 +174,9 @@ struct fc_ctx {
     bool step_big = false;             // FC_STEP=big: thread-per-row k_step_big for C > 32
     bool fuse_gram = false;            // FC_FUSE=1: fused k_step_gram for C <= 32 FISTA (measured slower: 8.5 vs 8.2 ms at C)
     bool tol = false;                  // fc_set_parity_mode(1): tolerance mode (FMA, single-gather FISTA)
+    bool step_t2 = false;              // FC_STEP=t2 / t2x: two-tile k_step_t2 (EXACT / runtime-C template)
+    bool step_t2_inexact = false;
+    bool step_inexact = false;         // FC_STEP=tx: k_step_t with the runtime-C template at C == G
     bool pair_sweep = false;           // FC_PAIR=1: C <= 8 dual sweep gathers interleaved [bar | prev] rows
                                        // (measured E8: 6.34 incl. pack vs 6.41 ms -- within noise, off)
     double* d_pair = nullptr;          // C <= 8: interleaved [bar | prev] rows, N x 2C
@@ -453,6 +456,24 @@ int launch_step_t(fc_ctx* ctx, const Bufs& b, const Geo& g) {
 }
 
 template <int G, bool EXACT>
+int launch_step_t2(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
+    const size_t smem = step_t2_smem(G);
+    if (!grid) {
+        CU(cudaFuncSetAttribute(k_step_t2<G, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_step_t2<G, EXACT>, kStepThreads, smem, ctx->sm_count);
+    }
+    const unsigned long long need = (g.nrows + 32 * (kStepThreads / 32) - 1) / (32 * (kStepThreads / 32));
+    const int gr = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(grid, need));
+    k_step_t2<G, EXACT><<<gr, kStepThreads, smem, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_step_t2 launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
+template <int G, bool EXACT>
 int launch_step_gram(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     static PerDevice<int> grid_pd;
     int& grid = grid_pd(ctx);
@@ -555,6 +576,10 @@ struct LaunchStep {
             if (ctx->tol)
                 return g.C == (unsigned)G ? launch_step_t<G, true, false, true>(ctx, b, g)
                                           : launch_step_t<G, false, false, true>(ctx, b, g);
+            if (ctx->step_t2)
+                return g.C == (unsigned)G && !ctx->step_t2_inexact ? launch_step_t2<G, true>(ctx, b, g)
+                                                                   : launch_step_t2<G, false>(ctx, b, g);
+            if (ctx->step_inexact) return launch_step_t<G, false, false>(ctx, b, g);
             return g.C == (unsigned)G ? launch_step_t<G, true, false>(ctx, b, g)
                                       : launch_step_t<G, false, false>(ctx, b, g);
         }
@@ -1305,6 +1330,9 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
     if (const char* sp = std::getenv("FC_STEP")) {
         ctx->step_big = std::strcmp(sp, "big") == 0;
         ctx->step_wide2 = std::strcmp(sp, "wide1") != 0;
+        ctx->step_t2 = std::strcmp(sp, "t2") == 0 || std::strcmp(sp, "t2x") == 0;
+        ctx->step_t2_inexact = std::strcmp(sp, "t2x") == 0;
+        ctx->step_inexact = std::strcmp(sp, "tx") == 0;
     }
     if (const char* fu = std::getenv("FC_FUSE")) ctx->fuse_gram = std::strcmp(fu, "1") == 0;
     if (const char* ha = std::getenv("FC_HALO")) ctx->halo_mode = std::atoi(ha);

@@ -1967,7 +1967,7 @@ __device__ __forceinline__ void stage_gram_matrix(const Bufs& b, double* Gr, int
 // and TX the new rows bar^n (already stored to D).  Returns false on a non-finite y.
 // BT: also the backtracking row terms (as k_step): lin_i = sum_r g_r (bar_r - x_r),
 // sq_i = sum_r (bar_r - x_r)^2, <xs_i, x_i>; g is parked in the thread's A-tile row.
-template <int G, bool EXACT, bool BT, bool TOL = false>
+template <int G, bool EXACT, bool BT, bool TOL = false, bool NO_TB = false>
 __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, const Geo& g, const double* Gr,
                                              int C, double* TA, double* TB, double* TX, unsigned long long rb,
                                              unsigned long long rend) {
@@ -1994,7 +1994,7 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
             const size_t a = (size_t)(g.row0 + row) * C + lg;
             const int t = (p + sub) * LD + lg;
             cp_async8(TA + t, A + a);
-            if (mode != kLiteral) cp_async8(TB + t, Bp + a);
+            if (!NO_TB && mode != kLiteral) cp_async8(TB + t, Bp + a);
             cp_async8(TX + t, XS + (size_t)row * C + lg);
         }
     }
@@ -2003,9 +2003,25 @@ __device__ __forceinline__ bool step_t_batch(const StepPlan& sp, const Bufs& b, 
     __syncwarp();
     double xr[G];
     if (row_ok) {
+        if constexpr (NO_TB) {
+            // bar^{n-2} straight from global into registers, thread per row (no B tile:
+            // a third less shared memory per warp, one more CTA per SM)
+            const double* brow = Bp + (size_t)(g.row0 + rb + lane) * C;
 #pragma unroll
-        for (int l = 0; l < G; ++l)
-            xr[l] = (EXACT || l < C) ? ((mode == kLiteral) ? ra[l] : extrap(ra[l], rb_[l], sp.beta)) : 0.0;
+            for (int l = 0; l < G; ++l) xr[l] = (EXACT || l < C) ? ra[l] : 0.0;
+            if (mode != kLiteral) {
+                double bv[G];
+#pragma unroll
+                for (int l = 0; l < G; ++l) bv[l] = (EXACT || l < C) ? ldg(brow + l) : 0.0;
+#pragma unroll
+                for (int l = 0; l < G; ++l)
+                    if (EXACT || l < C) xr[l] = extrap(xr[l], bv[l], sp.beta);
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < G; ++l)
+                xr[l] = (EXACT || l < C) ? ((mode == kLiteral) ? ra[l] : extrap(ra[l], rb_[l], sp.beta)) : 0.0;
+        }
     }
     if constexpr (TOL) {
         // S X_ext = S bar + beta (S bar - S bar_prev): S bar_prev rows into the B tile,
@@ -2133,6 +2149,36 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step_t(Bufs b, Geo g) {
     bool ok = true;
     for (unsigned long long rb = w0 * 32; rb < g.nrows; rb += warps * 32)
         ok = step_t_batch<G, EXACT, BT, TOL>(sp, b, g, Gr, C, TA, TB, TX, rb, g.nrows) && ok;
+    if (!ok) {
+        st->error = 1;
+        st->done = 1;
+    }
+}
+
+// K3 variant with two tiles per warp (A and S X_ext; bar^{n-2} read per thread): 75 KB of
+// shared memory per 4-warp CTA, so three CTAs (12 warps) fit an SM when the registers
+// allow (launch bound 128 x 3).  FC_STEP=t2 (C <= 32, no backtracking, bitwise).
+inline size_t step_t2_smem(int G) { return sizeof(double) * ((size_t)G * G + (kStepThreads / 32) * 2 * 32 * (G + 1)); }
+
+template <int G, bool EXACT>
+__global__ void __launch_bounds__(kStepThreads, 3) k_step_t2(Bufs b, Geo g) {
+    DevState* st = b.st;
+    if (st->done) return;
+    extern __shared__ double smt[];
+    constexpr int LD = G + 1;
+    const int C = EXACT ? G : (int)g.C;
+    const int warp = threadIdx.x >> 5;
+    double* Gr = smt;
+    double* TA = smt + G * G + warp * 2 * 32 * LD;
+    double* TX = TA + 32 * LD;
+    const StepPlan sp = step_plan(b);
+    stage_gram_matrix<G>(b, Gr, C);
+    __syncthreads();
+    const unsigned long long warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    bool ok = true;
+    for (unsigned long long rb = w0 * 32; rb < g.nrows; rb += warps * 32)
+        ok = step_t_batch<G, EXACT, false, false, true>(sp, b, g, Gr, C, TA, TA, TX, rb, g.nrows) && ok;
     if (!ok) {
         st->error = 1;
         st->done = 1;

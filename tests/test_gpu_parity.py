@@ -469,3 +469,21 @@ def test_pair_layout_sweep_bitwise(oracle, monkeypatch, c, vshards):
             assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("variant", ["t2", "t2x", "tx"])
+@pytest.mark.parametrize("c", [3, 16, 20, 32])
+def test_step_t_variants_bitwise(oracle, monkeypatch, variant, c):
+    """FC_STEP=t2 / t2x (two tiles per warp, bar^{n-2} read per thread, 3 CTAs per SM) and
+    tx (runtime-C template at C == G): FISTA with restart and GPA bitwise vs the oracle."""
+    monkeypatch.setenv("FC_STEP", variant)
+    g = random_graph(7000, 9.0, 70 + c)
+    x0 = oracle.init_random(g.n, c, 3)
+    t = capi.Context(0)
+    try:
+        t.upload(g)
+        for kw in (dict(method=FISTA, max_iter=8, fista_restart=True, step_size=40 * oracle.default_step_size(g)),
+                   dict(method=GPA, max_iter=5)):
+            assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+    finally:
+        t.close()
