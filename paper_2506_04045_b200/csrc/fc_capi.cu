@@ -712,11 +712,12 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
     const size_t N = ctx->n, L = ctx->local_rows, LB = ctx->local_blocks;
     for (int k = 0; k < 3; ++k) TRY(dalloc(ctx, &ctx->d_U[k], N * c));
     for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_xs[k], L * c));
-    // backtracking-only buffers exist exactly when bt_alloc is set (a non-backtracking
-    // re-allocation frees them, so no stale, smaller copy survives a change of C)
+    // backtracking-only buffers are valid (sized for this C) exactly when bt_alloc is set; a
+    // non-backtracking re-allocation keeps any older ones allocated but invalid (freeing them
+    // here would put a synchronising cudaFree into the next solve), and the checkpoint layout
+    // follows the header's flag, not the pointers (for_session_buffers)
     for (int k = 2; k < 4; ++k) {
         if (bt) TRY(dalloc(ctx, &ctx->d_xs[k], L * c));
-        else dfree(ctx, &ctx->d_xs[k]);
     }
     TRY(dalloc(ctx, &ctx->d_prod, L));
     if (ctx->pair_sweep && c <= 8) TRY(dalloc(ctx, &ctx->d_pair, N * 2 * c));
@@ -727,7 +728,6 @@ int ensure_work(fc_ctx* ctx, uint32_t c, bool bt) {
     }
     for (int k = 0; k < 3; ++k) {
         if (bt) TRY(dalloc(ctx, &ctx->d_rowterm[k], L));
-        else dfree(ctx, &ctx->d_rowterm[k]);
     }
     const unsigned np = npairs_of(c);
     for (int k = 0; k < 2; ++k) TRY(dalloc(ctx, &ctx->d_gpart[k], LB * np));
