@@ -20,7 +20,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <cstring>
 #include <condition_variable>
 #include <cstdint>
 #include <cstdio>
@@ -57,14 +60,55 @@ inline int transport_fail(std::string* err, const char* what, const char* detail
 struct NcclTransport final : Transport {
     ncclComm_t comm;
     int rank, world;
-    NcclTransport(ncclComm_t c, int r, int w) : comm(c), rank(r), world(w) {}
-    ~NcclTransport() override { ncclCommDestroy(comm); }
+    NcclTransport(ncclComm_t c, int r, int w) : comm(c), rank(r), world(w) {
+        if (const char* a = std::getenv("FC_ALLGATHER")) padded = std::strcmp(a, "padded") == 0;
+    }
+    ~NcclTransport() override {
+        if (staging) cudaFree(staging);
+        ncclCommDestroy(comm);
+    }
     const char* name() const override { return "nccl"; }
     static int chk(ncclResult_t r, std::string* err, const char* what) {
         return r == ncclSuccess ? 0 : transport_fail(err, what, ncclGetErrorString(r));
     }
+    // FC_ALLGATHER=padded: one ncclAllGather of max-shard-sized slices into a staging
+    // buffer, then device copies to each owner's row offset (NCCL's allgather algorithms --
+    // ring / NVLS -- for one padded collective, at the price of one extra N x C device copy)
+    bool padded = false;
+    double* staging = nullptr;
+    size_t staging_cap = 0;
+    int allgather_padded(double* buf, const uint64_t* bounds, uint32_t c, cudaStream_t s, std::string* err) {
+        uint64_t maxrows = 0;
+        for (int r = 0; r < world; ++r) maxrows = std::max<uint64_t>(maxrows, bounds[r + 1] - bounds[r]);
+        const size_t slice = maxrows * c, need = slice * world;
+        if (need > staging_cap) {
+            if (staging) cudaFree(staging);
+            staging = nullptr;
+            staging_cap = 0;
+            const cudaError_t e = cudaMalloc(&staging, std::max<size_t>(need, 1) * sizeof(double));
+            if (e != cudaSuccess) return transport_fail(err, "padded allgather staging", cudaGetErrorString(e));
+            staging_cap = need;
+        }
+        const size_t own = (bounds[rank + 1] - bounds[rank]) * c;
+        cudaError_t e = cudaMemcpyAsync(staging + rank * slice, buf + bounds[rank] * c, own * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return transport_fail(err, "padded allgather copy", cudaGetErrorString(e));
+        if (int x = chk(ncclAllGather(staging + rank * slice, staging, slice, ncclDouble, comm, s), err,
+                        "ncclAllGather"))
+            return x;
+        for (int r = 0; r < world; ++r) {
+            if (r == rank) continue;
+            const size_t cnt = (bounds[r + 1] - bounds[r]) * c;
+            if (!cnt) continue;
+            e = cudaMemcpyAsync(buf + bounds[r] * c, staging + r * slice, cnt * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return transport_fail(err, "padded allgather scatter", cudaGetErrorString(e));
+        }
+        return 0;
+    }
     // unequal shards: one broadcast per owner, grouped (NCCL allgather needs equal counts)
     int allgather_rows(double* buf, const uint64_t* bounds, uint32_t c, cudaStream_t s, std::string* err) override {
+        if (padded) return allgather_padded(buf, bounds, c, s, err);
         if (int e = chk(ncclGroupStart(), err, "ncclGroupStart")) return e;
         for (int r = 0; r < world; ++r) {
             const size_t off = bounds[r] * c, cnt = (bounds[r + 1] - bounds[r]) * c;

@@ -288,18 +288,22 @@ def test_tma_sweep_variant_bitwise(oracle, n, c, monkeypatch):
 
 
 # ---- the NCCL code path on one GPU (1-rank communicator) ------------------------------------
-def test_nccl_path_single_rank_bitwise(oracle, monkeypatch):
-    """FC_FORCE_NCCL=1 runs the multi-GPU schedule (grouped-broadcast allgather,
-    recv -> combine -> send -> broadcast chain) through a real 1-rank NCCL
-    communicator; results must stay bitwise equal to the oracle."""
+@pytest.mark.parametrize("allgather", ["grouped", "padded"])
+def test_nccl_path_single_rank_bitwise(oracle, monkeypatch, allgather):
+    """FC_FORCE_NCCL=1 runs the multi-GPU schedule (grouped-broadcast or padded
+    ncclAllGather, recv -> combine -> send -> broadcast chain, FISTA + backtracking with
+    the per-pass plan read) through a real 1-rank NCCL communicator; results must stay
+    bitwise equal to the oracle."""
     monkeypatch.setenv("FC_FORCE_NCCL", "1")
+    monkeypatch.setenv("FC_ALLGATHER", allgather)
     t = capi.Context(0, rank=0, world=1, nccl_id=capi.nccl_unique_id())
     try:
         g = random_graph(6000, 7.0, 31)
         t.upload(g)
         x0 = oracle.init_random(g.n, 16, 4)
         for kw in [dict(method=GPA, max_iter=10), dict(method=FISTA, max_iter=10, fista_restart=True),
-                   dict(method=FISTA, max_iter=10, step_size=40 * oracle.default_step_size(g))]:
+                   dict(method=FISTA, max_iter=10, step_size=40 * oracle.default_step_size(g)),
+                   dict(method=FISTA_BT, max_iter=6, step_size=300 * oracle.default_step_size(g))]:
             assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
         with pytest.raises(fc.InvalidInput, match="single-rank"):
             t.share_matrix(x0)
