@@ -841,7 +841,7 @@ int phase_gram(fc_ctx* ctx, bool dual, cudaStream_t strm = nullptr, unsigned max
     size_t (&smem_set)[128] = smem_set_pd(ctx);
     auto pick = [&](auto tol) {
         constexpr bool T = decltype(tol)::value;
-        return TS == 1 ? k_gram<1, 1, T> : TS == 8 ? k_gram_wide<8, 8, T> : TS == 48 ? k_gram_wide<4, 8, T> : k_gram<4, 4, T>;
+        return TS == 1 ? k_gram<1, 1, T> : TS == 8 ? k_gram<8, 8, T> : TS == 48 ? k_gram<4, 8, T> : k_gram<4, 4, T>;
     };
     auto kfn = ctx->tol ? pick(std::true_type{}) : pick(std::false_type{});
     const int sidx = (TS % 64) + (ctx->tol ? 64 : 0);

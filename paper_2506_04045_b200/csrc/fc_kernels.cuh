@@ -1084,25 +1084,8 @@ __host__ __device__ inline size_t gram_smem(int C, int dual, int R, int TS = 4) 
 // TS x TS register tiles: TS = 4 in general; TS = 1 when there are few 1024-row
 // blocks (small N): every (r, s) pair gets its own thread, so the 1024-long
 // sequential chains of all pairs run in parallel instead of 16 per thread.
-template <int TR, int TC, bool TOL>
-__device__ __forceinline__ void gram_body(Bufs& b, Geo& g, int dual, int rows_per_chunk);
-
-// 4x4 (and 1x1) tiles: at most 320 threads per CTA, registers as the launch bound allows
 template <int TR, int TC = TR, bool TOL = false>
 __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dual, int rows_per_chunk) {
-    gram_body<TR, TC, TOL>(b, g, dual, rows_per_chunk);
-}
-
-// 8x8 tiles (C >= 64): 64 accumulators per thread; a 200-register budget lets the compiler
-// keep several products in flight (at the 168 it chose under the launch bound every DMUL
-// fed its DADD back to back: fixed-latency stalls)
-template <int TR, int TC = TR, bool TOL = false>
-__global__ void __maxnreg__(200) k_gram_wide(Bufs b, Geo g, int dual, int rows_per_chunk) {
-    gram_body<TR, TC, TOL>(b, g, dual, rows_per_chunk);
-}
-
-template <int TR, int TC, bool TOL>
-__device__ __forceinline__ void gram_body(Bufs& b, Geo& g, int dual, int rows_per_chunk) {
     const DevState* st = b.st;
     if (st->done) return;
     extern __shared__ double smg[];
@@ -1205,21 +1188,9 @@ __device__ __forceinline__ void gram_body(Bufs& b, Geo& g, int dual, int rows_pe
                     for (int a = 0; a < TC; ++a) xq[a] = t[rr * C4 + TC * J + a];
                 }
 #pragma unroll
-                for (int a = 0; a < TR; ++a) {
-                    if constexpr (TOL) {
+                for (int a = 0; a < TR; ++a)
 #pragma unroll
-                        for (int c = 0; c < TC; ++c) acc[a][c] = madd<TOL>(acc[a][c], xr[a], xq[c]);
-                    } else {
-                        // the row's TC products first, then the TC additions: independent DMULs
-                        // in flight instead of DMUL -> dependent DADD pairs (same values, same order
-                        // per accumulator)
-                        double p[TC];
-#pragma unroll
-                        for (int c = 0; c < TC; ++c) p[c] = dmul(xr[a], xq[c]);
-#pragma unroll
-                        for (int c = 0; c < TC; ++c) acc[a][c] = dadd(acc[a][c], p[c]);
-                    }
-                }
+                    for (int c = 0; c < TC; ++c) acc[a][c] = madd<TOL>(acc[a][c], xr[a], xq[c]);
             }
         }
         __syncthreads();                                     // stage sidx is re-filled next round
