@@ -497,8 +497,10 @@ def main():
     peak, peak_kind = peaks()
     lo, hi = (int(bounds[rank]), int(bounds[rank + 1])) if world > 1 else (0, graph.n)
     nnz_l = int(graph.row_ptr[hi] - graph.row_ptr[lo])
-    it_b_total, _ = bytes_model(graph.n, graph.nnz, cfg["c"], cfg["method"])
-    _, sweep_b = bytes_model(hi - lo, nnz_l, cfg["c"], cfg["method"])
+    # tolerance mode gathers one operand per FISTA sweep (the GPA byte model)
+    bm = "gpa" if args.parity_mode == 1 else cfg["method"]
+    it_b_total, _ = bytes_model(graph.n, graph.nnz, cfg["c"], bm)
+    _, sweep_b = bytes_model(hi - lo, nnz_l, cfg["c"], bm)
     sweep_ms, sweep_n = kt["sweep"]
     sweep_avg = sweep_ms / max(1, sweep_n)
     if prof_iters != args.steps:                       # converged during the breakdown pass: no-op launches

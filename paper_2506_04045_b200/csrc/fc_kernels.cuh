@@ -400,12 +400,25 @@ struct SweepTune {
     static constexpr int MINB = G == 32 ? (S == 1 ? 3 : 2) : (G == 16 ? FC_SWEEP16_MINB : 4);   // CTAs per SM
 };
 
+// Single-gather sweeps (GPA, prelude, tolerance-mode FISTA) gather one operand and keep
+// half the dual sweep's loads in flight.  -DFC_SWEEP1_WIDE=1 gives them 2U at 2 CTAs per
+// SM: measured slower (tolerance-mode C sweep 19.7 vs 16.7-17.5 ms), so off.
+#ifndef FC_SWEEP1_WIDE
+#define FC_SWEEP1_WIDE 0
+#endif
+template <int G, int S, bool DUAL>
+struct SweepTuneD {
+    static constexpr bool WIDE = !DUAL && G == 32 && FC_SWEEP1_WIDE;
+    static constexpr int U = WIDE ? 2 * SweepTune<G, S>::U : SweepTune<G, S>::U;
+    static constexpr int MINB = WIDE ? 2 : SweepTune<G, S>::MINB;
+};
+
 template <int G, int S, bool DUAL, bool W, bool EXACT>
 __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const double* __restrict__ P, double beta,
                                             unsigned myidx, double myw, int cnt, unsigned gmask, unsigned lg,
                                             unsigned C, double (&ab)[S], double (&ae)[S], unsigned long long pol_hot,
                                             unsigned long long pol_cold, unsigned long long N) {
-    constexpr int U = SweepTune<G, S>::U;
+    constexpr int U = SweepTuneD<G, S, DUAL>::U;
     if (cnt == G) {
 #pragma unroll
         for (int k0 = 0; k0 < G; k0 += U) {
@@ -483,7 +496,7 @@ __device__ __forceinline__ void sweep_chunk(const double* __restrict__ B, const 
 // a power-law hub (114k entries at config C) is one sequential chain per
 // component, and started late it would set the kernel's tail.
 template <int G, int S, bool DUAL, bool W, bool EXACT>
-__global__ void __launch_bounds__(256, SweepTune<G, S>::MINB) k_sweep(Bufs b, Geo g) {
+__global__ void __launch_bounds__(256, SweepTuneD<G, S, DUAL>::MINB) k_sweep(Bufs b, Geo g) {
     const DevState* st = b.st;
     if (st->done) return;
     const unsigned kChunk = g.chunk;                        // rows per counter grab (<= 32)
