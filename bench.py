@@ -499,7 +499,9 @@ def main():
     nnz_l = int(graph.row_ptr[hi] - graph.row_ptr[lo])
     # tolerance mode gathers one operand per FISTA sweep (the GPA byte model)
     bm = "gpa" if args.parity_mode == 1 else cfg["method"]
-    it_b_total, _ = bytes_model(graph.n, graph.nnz, cfg["c"], bm)
+    it_b_total, _ = bytes_model(graph.n, graph.nnz, cfg["c"], cfg["method"])
+    if args.parity_mode == 1 and cfg["method"] != "gpa":   # one gather per sweep, six N x C streams
+        it_b_total = 8 * (graph.n + 1) + 12 * graph.nnz + 8 * cfg["c"] * graph.nnz + 6 * 8 * cfg["c"] * graph.n
     _, sweep_b = bytes_model(hi - lo, nnz_l, cfg["c"], bm)
     sweep_ms, sweep_n = kt["sweep"]
     sweep_avg = sweep_ms / max(1, sweep_n)
