@@ -913,20 +913,15 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
                             const double v = ok ? ldg(b.pair + (size_t)(raw & kIdxMask) * (2 * C) + poff) : 0.0;
                             const double pv = __shfl_down_sync(kFull, v, G);
                             const double ev = extrap(v, pv, beta);
-                            ve[u] = W ? dmul(w, ev) : ev;
-                            vb[u] = W ? dmul(w, v) : v;
+                            ve[u] = ok ? (W ? dmul(w, ev) : ev) : -0.0;     // -0.0: exact no-op addend
+                            vb[u] = ok ? (W ? dmul(w, v) : v) : -0.0;
                         }
 #pragma unroll
                         for (int u = 0; u < UP; ++u) {
 #pragma unroll
                             for (int qq = 0; qq < QP; ++qq) {
-                                const int k = t0 + u * QP + qq;
-                                const double bb = __shfl_sync(kFull, vb[u], qq * GP + c);
-                                const double ee = __shfl_sync(kFull, ve[u], qq * GP + c);
-                                if (k < cnt) {
-                                    ab = dadd(ab, bb);
-                                    ae = dadd(ae, ee);
-                                }
+                                ab = dadd(ab, __shfl_sync(kFull, vb[u], qq * GP + c));
+                                ae = dadd(ae, __shfl_sync(kFull, ve[u], qq * GP + c));
                             }
                         }
                     }
@@ -941,24 +936,26 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
                         const bool ok = k < cnt && okc;
                         const unsigned o = (raw & kIdxMask) * C;
                         FC_DCHECK(!ok || (raw & kIdxMask) < g.N);
-                        double bv = ok ? ldg(B + o) : 0.0;
+                        const double bv = ok ? ldg(B + o) : 0.0;
                         if (DUAL) {
                             const double pv = ok ? ldg(P + o) : 0.0;
                             const double ev = extrap(bv, pv, beta);
-                            ve[u] = W ? dmul(w, ev) : ev;
+                            ve[u] = ok ? (W ? dmul(w, ev) : ev) : -0.0;
                         }
-                        vb[u] = W ? dmul(w, bv) : bv;
+                        vb[u] = ok ? (W ? dmul(w, bv) : bv) : -0.0;
                     }
+                    // slots past the row's end hold -0.0, and x + (-0.0) == x for every x in
+                    // round-to-nearest (+0 + -0 = +0, -0 + -0 = -0): the additions are
+                    // unconditional (no per-slot select) and the chains stay bitwise
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
 #pragma unroll
                         for (int qq = 0; qq < Q; ++qq) {
-                            const int k = t0 + u * Q + qq;
                             const double bb = __shfl_sync(kFull, vb[u], qq * G + c);
-                            const double ee = DUAL ? __shfl_sync(kFull, ve[u], qq * G + c) : 0.0;
-                            if (k < cnt) {
-                                ab = dadd(ab, bb);
-                                if (DUAL) ae = dadd(ae, ee);
+                            ab = dadd(ab, bb);
+                            if (DUAL) {
+                                const double ee = __shfl_sync(kFull, ve[u], qq * G + c);
+                                ae = dadd(ae, ee);
                             }
                         }
                     }
