@@ -178,6 +178,7 @@ struct fc_ctx {
     bool step_t2_inexact = false;
     bool step_inexact = false;         // FC_STEP=tx: k_step_t with the runtime-C template at C == G
     bool pair_sweep = false;           // FC_PAIR=1: C <= 8 dual sweep gathers interleaved [bar | prev] rows
+    int sweep_async = 0;               // FC_ASYNC=3|4|6: the PAIR sweep through a cp.async ring of S stages
                                        // (measured E8: 6.34 incl. pack vs 6.41 ms -- within noise, off)
     double* d_pair = nullptr;          // C <= 8: interleaved [bar | prev] rows, N x 2C
     bool step_wide2 = true;            // FC_STEP=wide1: the round-1 k_step_wide (G streamed) for 32 < C <= 128
@@ -406,6 +407,23 @@ int launch_sweep_small_pair(fc_ctx* ctx, const Bufs& b, const Geo& g) {
     return FC_OK;
 }
 
+template <int G, bool W, int S>
+int launch_sweep_async(fc_ctx* ctx, const Bufs& b, const Geo& g) {
+    constexpr int U = G < 8 ? G : 8;
+    static PerDevice<int> grid_pd;
+    int& grid = grid_pd(ctx);
+    const size_t smem = sizeof(SweepRing<G, W, S, U>) * (128 / G);
+    if (!grid) {
+        CU(cudaFuncSetAttribute(k_sweep_async<G, W, S, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = grid_for((const void*)k_sweep_async<G, W, S, U>, 128, smem, ctx->sm_count);
+    }
+    k_sweep_async<G, W, S, U><<<grid, 128, smem, ctx->stream>>>(b, g);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(ctx, FC_DEVICE, "k_sweep_async launch: %s", cudaGetErrorString(e));
+    return FC_OK;
+}
+
 template <int G, int S>
 struct LaunchSweep {
     static int run(fc_ctx* ctx, const Bufs& b, const Geo& g, bool dual) {
@@ -413,6 +431,15 @@ struct LaunchSweep {
         if constexpr (G <= 8) {   // measured: C=8 9.5 vs 12.2 ms (E8); C=16 keeps the group sweep (B: 1.52 vs 1.78 ms)
             if (!ctx->sweep_groups) {
                 const bool w = ctx->weighted;
+                if (dual && b.pair && ctx->sweep_async) {
+                    if constexpr (G == 8) {
+                        if (ctx->sweep_async == 3)
+                            return w ? launch_sweep_async<G, true, 3>(ctx, b, g) : launch_sweep_async<G, false, 3>(ctx, b, g);
+                        if (ctx->sweep_async == 6)
+                            return w ? launch_sweep_async<G, true, 6>(ctx, b, g) : launch_sweep_async<G, false, 6>(ctx, b, g);
+                    }
+                    return w ? launch_sweep_async<G, true, 4>(ctx, b, g) : launch_sweep_async<G, false, 4>(ctx, b, g);
+                }
                 if (dual && b.pair)
                     return w ? launch_sweep_small_pair<G, true>(ctx, b, g) : launch_sweep_small_pair<G, false>(ctx, b, g);
                 if (dual) return w ? launch_sweep_small<G, true, true>(ctx, b, g) : launch_sweep_small<G, true, false>(ctx, b, g);
@@ -1337,6 +1364,7 @@ static int create_common(fc_ctx** out, int device, int rank, int world, int vsha
     if (const char* fu = std::getenv("FC_FUSE")) ctx->fuse_gram = std::strcmp(fu, "1") == 0;
     if (const char* ha = std::getenv("FC_HALO")) ctx->halo_mode = std::atoi(ha);
     if (const char* pa = std::getenv("FC_PAIR")) ctx->pair_sweep = std::strcmp(pa, "1") == 0;
+    if (const char* sa = std::getenv("FC_ASYNC")) ctx->sweep_async = std::atoi(sa);
     if (const char* gr = std::getenv("FC_GRAPHS")) ctx->graphs = std::strcmp(gr, "0") != 0;
     {
         const unsigned hw = std::thread::hardware_concurrency();

@@ -833,8 +833,14 @@ __global__ void __launch_bounds__(kSwTmaThreads) k_sweep_tma(Bufs b, Geo g, cons
 // A warp owns a 32-row chunk and walks its rows in order; column indices of the
 // next 32 nonzeros are prefetched.
 // =============================================================================
-template <int G, bool DUAL, bool W, bool PAIR>
-__device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
+struct NoLightChunk {
+    __device__ void operator()(unsigned long long, unsigned) const {}
+};
+
+// MODE 0: heavy rows, then every chunk through strip(); MODE 2: chunks without a heavy
+// row go to light(base, nr) instead (k_sweep_async)
+template <int G, bool DUAL, bool W, bool PAIR, int MODE = 0, class Light = NoLightChunk>
+__device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g, Light light = Light()) {
     const DevState* st = b.st;
     if (st->done) return;
 
@@ -997,6 +1003,18 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g) {
             rb = base;
             nrow = (unsigned)min((unsigned long long)kChunk, g.nrows - base);
             tdeg = heavy_deg;
+            if (MODE == 2) {
+                bool hv = false;
+                if (tdeg != LLONG_MAX) {
+                    const long long a0 = __ldg(b.row_ptr + rb + min(lane, nrow));
+                    const long long a1 = __ldg(b.row_ptr + rb + min(lane + 1, nrow));
+                    hv = __any_sync(kFull, a1 - a0 >= tdeg);
+                }
+                if (!hv) {
+                    light(rb, nrow);
+                    continue;
+                }
+            }
         }
         strip(rb, nrow, tdeg);
     }
@@ -1015,6 +1033,197 @@ __global__ void __launch_bounds__(256, 4) k_sweep_small(Bufs b, Geo g) {
 template <int G, bool W>
 __global__ void __launch_bounds__(256, 4) k_sweep_small_pair(Bufs b, Geo g) {
     k_sweep_small_body<G, true, W, true>(b, g);
+}
+
+// =============================================================================
+// K1 async-copy variant (dual, C <= G <= 8, PAIR layout).  k_sweep_small's
+// gathers are register-staged (every nonzero in flight holds registers in 8-16
+// lanes) and its per-slot value shuffles + padded row tails cost ~32 warp
+// instructions per nonzero (ncu, E8).  Here G lanes form a group (lane =
+// component), each group owns G consecutive rows of the warp's 32-row chunk
+// and walks their nonzeros as ONE flat stream, staged through a shared-memory
+// ring with cp.async: S stages of U interleaved [bar | prev] rows (lane c
+// copies bytes [16c, 16c+16) of each 16C-byte row), the column indices copied
+// S stages ahead of the values, so S-1 stages are in flight per group without
+// holding registers and without an index load on the issue path.  The groups
+// of a warp advance in lockstep (warp-uniform stage loop; a group past its
+// stream is predicated off; row flushes under __any_sync), so the warp never
+// serialises divergent groups.  Per row: the same chains ab = sum w*bar,
+// ae = sum w*extrap(bar, prev) from 0.0 in CSR order as k_sweep_small (bitwise
+// identical).  Chunks holding a heavy row go through k_sweep_small's strip,
+// after the heavy phase.
+// =============================================================================
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int G, bool W, int S, int U>
+struct SweepRing {                                 // one per lane group
+    double val[S][U][2 * G];                       // stage slot: U rows [bar | prev] (2C of 2G used)
+    double w[W ? 2 * S : 1][U];                    // weights, with the indices
+    unsigned idx[2 * S][U];                        // column indices, S stages ahead of the values
+};
+
+// rows [base, base + nr) of the shard (nr <= 32, no heavy row among them).  Positions are
+// 32-bit offsets into the group's stream; a slot past the stream is zero-filled in shared
+// memory (weight 0): its addends are +0.0, and x + (+0.0) == x for every x != -0.0 -- the
+// chains start at +0.0 and a round-to-nearest sum is -0.0 only when both operands are, so
+// they never hold -0.0 and the padding is exact without per-slot selects.
+template <int G, bool W, int S, int U>
+__device__ __forceinline__ void sweep_async_chunk(Bufs& b, Geo& g, unsigned long long base, unsigned nr,
+                                                  SweepRing<G, W, S, U>& ring) {
+    static_assert(U <= G, "one index per lane per stage");
+    const DevState* st = b.st;
+    const unsigned C = g.C;
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned gi = lane / G, c = lane % G;
+    const unsigned r_lo = min(nr, gi * G), r_hi = min(nr, (gi + 1) * G);
+    const unsigned nrg = r_hi - r_lo;             // this group's rows (0 for idle groups)
+    const unsigned long long gbase = base + r_lo;
+    const bool okc = c < C;
+    const double beta = st->beta_next;
+    const double* __restrict__ Xown = b.U[st->sw_b] + c;
+    double* xs_main = b.xs[st->xs_w * 2 + kMatBar] + c;
+    double* xs_ext = b.xs[st->xs_w * 2 + kMatExt] + c;
+    const char* pairb = reinterpret_cast<const char*>(b.pair) + 16 * c;
+    const unsigned rowbytes = 16 * C;
+
+    const long long e0 = __ldg(b.row_ptr + gbase);
+    const unsigned my_end = c < nrg ? (unsigned)(__ldg(b.row_ptr + gbase + c + 1) - e0) : 0xffffffffu;
+    const unsigned last = __shfl_sync(kFull, my_end, nrg ? nrg - 1 : 0, G);
+    const unsigned len = nrg ? last : 0;          // stream length
+    const unsigned nst = (len + U - 1) / U;
+    unsigned nst_max = nst;
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) nst_max = max(nst_max, __shfl_xor_sync(kFull, nst_max, o));
+    const unsigned* __restrict__ colp = b.col + e0;
+    const double* __restrict__ valp = W ? b.val + e0 : nullptr;
+
+    auto issue_idx = [&](unsigned t) {             // column indices (and weights) of stage t
+        const unsigned k = t * U + c;
+        if (c < (unsigned)U) {
+            if (k < len) {
+                cp_async4(&ring.idx[t % (2 * S)][c], colp + k);
+                if (W) cp_async8(&ring.w[t % (2 * S)][c], valp + k);
+            } else if (W) {
+                ring.w[t % (2 * S)][c] = 0.0;
+            }
+        }
+    };
+    auto issue_val = [&](unsigned t) {             // the stage's rows; its indices have landed
+        const unsigned* ix = ring.idx[t % (2 * S)];
+        double* dst = &ring.val[t % S][0][2 * c];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!okc) continue;
+            if (t * U + u < len)
+                cp_async16(dst + u * 2 * G, pairb + (size_t)(ix[u] & kIdxMask) * rowbytes);
+            else                                   // past the stream: +0.0 addends
+                *reinterpret_cast<double2*>(dst + u * 2 * G) = make_double2(0.0, 0.0);
+        }
+    };
+    auto load_xi = [&](unsigned r) -> double {
+        return (okc && r < nrg) ? ldg(Xown + (size_t)(g.row0 + gbase + r) * C) : 0.0;
+    };
+    // flush row r of the groups with `need` (the shuffles run on every lane)
+    auto flush = [&](bool need, unsigned r, double ab, double ae, double xi) {
+        const unsigned long long row = gbase + r;
+        if (need && okc) {
+            xs_main[(size_t)row * C] = ab;
+            xs_ext[(size_t)row * C] = ae;
+        }
+        const double a = dmul(ab, xi);
+        double p = 0.0;
+#pragma unroll
+        for (int l2 = 0; l2 < G; ++l2) {
+            const double v = __shfl_sync(kFull, a, l2, G);
+            if ((unsigned)l2 < C) p = dadd(p, v);
+        }
+        if (need && c == 0) b.prod[row] = p;
+    };
+
+#pragma unroll
+    for (int t = 0; t < S; ++t) issue_idx(t);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+        if ((unsigned)t < nst_max) issue_val(t);
+        issue_idx(t + S);
+        cp_async_commit();
+    }
+    unsigned cur = 0;
+    unsigned cur_end = __shfl_sync(kFull, my_end, 0, G);
+    double xi = load_xi(0);
+    double ab = 0.0, ae = 0.0;
+    for (unsigned s = 0; s < nst_max; ++s) {
+        cp_async_wait<S - 1>();                    // stage s (and the indices of stage s + S) landed
+        __syncwarp();
+        const double* sv = &ring.val[s % S][0][c];
+        const double* sw = W ? ring.w[s % (2 * S)] : nullptr;
+        const unsigned k0 = s * U;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned k = k0 + u;
+            const double bv = sv[u * 2 * G];
+            const double pv = sv[u * 2 * G + C];
+            double xb = bv, xe = extrap(bv, pv, beta);
+            if (W) {
+                const double w = sw[u];
+                xb = dmul(w, xb);
+                xe = dmul(w, xe);
+            }
+            bool need = k == cur_end && cur < nrg;  // row `cur` ends before nonzero k (empty rows too)
+            while (__any_sync(kFull, need)) {
+                flush(need, cur, ab, ae, xi);
+                if (need) {
+                    ab = 0.0;
+                    ae = 0.0;
+                    ++cur;
+                }
+                cur_end = __shfl_sync(kFull, my_end, min(cur, (unsigned)G - 1u), G);
+                if (need) xi = load_xi(cur);
+                need = k == cur_end && cur < nrg;
+            }
+            ab = dadd(ab, xb);
+            ae = dadd(ae, xe);
+        }
+        __syncwarp();                              // slot s % S is free
+        if (s + S < nst_max) issue_val(s + S);
+        issue_idx(s + 2 * S);
+        cp_async_commit();
+    }
+    bool need = cur < nrg;                         // each group's last row, then trailing empty rows
+    while (__any_sync(kFull, need)) {
+        flush(need, cur, ab, ae, xi);
+        if (need) {
+            ab = 0.0;
+            ae = 0.0;
+            ++cur;
+            xi = load_xi(cur);
+        }
+        need = cur < nrg;
+    }
+    cp_async_wait<0>();                            // no copy may land in a ring the next chunk reuses
+    __syncwarp();
+}
+
+template <int G, bool W, int S, int U>
+__global__ void __launch_bounds__(128) k_sweep_async(Bufs b, Geo g) {
+    extern __shared__ __align__(16) unsigned char sweep_ring_smem[];
+    using Ring = SweepRing<G, W, S, U>;
+    Ring* ring = reinterpret_cast<Ring*>(sweep_ring_smem) + (threadIdx.x / G);
+    k_sweep_small_body<G, true, W, true, 2>(b, g, [&](unsigned long long base, unsigned nr) {
+        sweep_async_chunk<G, W, S, U>(b, g, base, nr, *ring);
+    });
 }
 
 // Interleave [bar^n | bar^{n-1}] rows for the PAIR sweep (after the row exchange).

@@ -475,6 +475,52 @@ def test_pair_layout_sweep_bitwise(oracle, monkeypatch, c, vshards):
         t.close()
 
 
+def ragged_graph(n, seed, weighted):
+    """Power-law degrees, two hubs, ~5% empty rows (no diagonal either), optional weights."""
+    from paper_2506_04045_b200 import SparseSimilarity
+    rng = np.random.default_rng(seed)
+    deg = np.minimum(rng.zipf(1.8, n), 400)
+    u = np.repeat(np.arange(n), deg)
+    v = rng.integers(0, n, len(u))
+    hubs = np.concatenate([np.full(n // 2, 7), np.full(n // 3, n - 5)])
+    u = np.concatenate([u, hubs])
+    v = np.concatenate([v, rng.integers(0, n, len(hubs))])
+    empty = rng.random(n) < 0.05
+    empty[[7, n - 5]] = False
+    k = (u != v) & ~empty[u] & ~empty[v]
+    e = np.unique(np.sort(np.stack([u[k], v[k]], 1), 1), axis=0)
+    ids = np.flatnonzero(~empty)
+    w = rng.uniform(0.1, 2.0, len(e)) if weighted else np.ones(len(e))
+    d = rng.uniform(0.5, 1.5, len(ids)) if weighted else np.ones(len(ids))
+    t = np.concatenate([np.stack([ids, ids, d], 1), np.stack([e[:, 0], e[:, 1], w], 1),
+                        np.stack([e[:, 1], e[:, 0], w], 1)])
+    return SparseSimilarity.from_triplets(n, t)
+
+
+@pytest.mark.parametrize("variant", ["FC_ASYNC=3", "FC_ASYNC=4", "FC_ASYNC=6"])
+@pytest.mark.parametrize("c", [1, 3, 8])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_stream_sweep_bitwise(oracle, monkeypatch, variant, c, weighted):
+    """FC_PAIR=1 FC_ASYNC=S (k_sweep_async: per-group flat nonzero streams staged through an
+    S-stage cp.async ring, warp-uniform) on a ragged graph (power-law degrees, hubs, empty rows), heavy rows through the
+    warp-cooperative phase (FC_HEAVY_DEG=64): FISTA with restart and with backtracking
+    bitwise equal to the oracle."""
+    monkeypatch.setenv("FC_PAIR", "1")
+    k, v = variant.split("=")
+    monkeypatch.setenv(k, v)
+    monkeypatch.setenv("FC_HEAVY_DEG", "64")
+    g = ragged_graph(7000, 90 + c, weighted)
+    x0 = oracle.init_random(g.n, c, 4)
+    t = capi.Context(0)
+    try:
+        t.upload(g)
+        for kw in (dict(method=FISTA, max_iter=8, fista_restart=True, step_size=40 * oracle.default_step_size(g)),
+                   dict(method=FISTA_BT, max_iter=5, step_size=300 * oracle.default_step_size(g))):
+            assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+    finally:
+        t.close()
+
+
 @pytest.mark.parametrize("variant", ["t2", "t2x", "tx"])
 @pytest.mark.parametrize("c", [3, 16, 20, 32])
 def test_step_t_variants_bitwise(oracle, monkeypatch, variant, c):
