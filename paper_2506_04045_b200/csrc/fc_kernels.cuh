@@ -15,6 +15,7 @@
 //   xs : shard rows x C f64 (S U products), two slots (0 = extrapolated point, 1 = bar).
 //   per-1024-row-block partials: Gram (packed upper triangle) and scalar terms.
 #pragma once
+#include <type_traits>
 
 #include <cstdint>
 #include <cuda.h>
@@ -932,10 +933,14 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g, Light light 
                         }
                     }
                 } else {
-                for (int t0 = 0; t0 < cnt; t0 += Q * U) {
-                    double vb[U], ve[DUAL ? U : 1];
+                // one batch = UU load slots per lane = Q * UU nonzeros; a row's last batch
+                // shrinks to the half / quarter batch that covers its remainder (fewer
+                // padded slots: shuffles and adds are per slot, not per nonzero)
+                auto batch = [&](auto uc, const int t0) {
+                    constexpr int UU = decltype(uc)::value;
+                    double vb[UU], ve[DUAL ? UU : 1];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
+                    for (int u = 0; u < UU; ++u) {
                         const int k = t0 + u * Q + (int)q;           // this lane's nonzero slot
                         const unsigned raw = __shfl_sync(kFull, myidx, k & 31);
                         const double w = W ? __shfl_sync(kFull, myw, k & 31) : 1.0;
@@ -954,7 +959,7 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g, Light light 
                     // round-to-nearest (+0 + -0 = +0, -0 + -0 = -0): the additions are
                     // unconditional (no per-slot select) and the chains stay bitwise
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
+                    for (int u = 0; u < UU; ++u) {
 #pragma unroll
                         for (int qq = 0; qq < Q; ++qq) {
                             const double bb = __shfl_sync(kFull, vb[u], qq * G + c);
@@ -964,6 +969,18 @@ __device__ __forceinline__ void k_sweep_small_body(Bufs& b, Geo& g, Light light 
                                 ae = dadd(ae, ee);
                             }
                         }
+                    }
+                };
+                int t0 = 0;
+                for (; cnt - t0 > Q * U / 2; t0 += Q * U) batch(std::integral_constant<int, U>{}, t0);
+                if (t0 < cnt) {
+                    if constexpr (U >= 4) {
+                        if (cnt - t0 > Q * U / 4) batch(std::integral_constant<int, U / 2>{}, t0);
+                        else batch(std::integral_constant<int, U / 4>{}, t0);
+                    } else if constexpr (U == 2) {
+                        batch(std::integral_constant<int, 1>{}, t0);
+                    } else {
+                        batch(std::integral_constant<int, U>{}, t0);
                     }
                 }
                 }
