@@ -100,7 +100,7 @@ struct fc_ctx {
     cudaStream_t side = nullptr;       // Gram next to the sweep (independent within an iteration)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool overlap = false;              // FC_OVERLAP=1: Gram on a side stream (measured: no gain)
-    int gram_ctas = 0;                 // FC_GRAM_CTAS: persistent Gram grid (0: 3/4 x overlap2 x SMs)
+    int gram_ctas = 0;                 // FC_GRAM_CTAS: persistent Gram grid (0: overlap2 x SMs, x 3/4 at C > 16)
     int overlap2 = 1;                  // persistent Gram (k CTAs per SM) launched before the sweep on a side
                                        // stream (default k = 1; FC_OVERLAP=0 disables, =2:k sets k)
     fc::Transport* xport = nullptr;    // multi-rank collectives (NCCL or in-process loopback); null = one rank
@@ -1025,11 +1025,13 @@ static int exchange_gram_sweep(fc_ctx* ctx, int buf, bool dual_sweep) {
     if (ctx->overlap2 && !ctx->profiling) {
         CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
         CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
-        // three quarters of the SMs: on the others the sweep keeps all its CTAs (a Gram CTA
-        // displaces one sweep CTA where it lands; measured C 38.1-38.4 -> 37.1-37.7 ms,
-        // E128 94.3 -> 87.1 ms vs one Gram CTA on every SM)
+        // C > 16: three quarters of the SMs, so the others keep the whole G = 32 sweep (a
+        // Gram CTA displaces one of its three CTAs where it lands; measured C 38.1-38.4 ->
+        // 37.1-37.7 ms, E128 94.3 -> 87.1 ms).  C <= 16 (k_sweep_small, G = 16 sweep): every
+        // SM (B 3.04-3.09 vs 2.81-2.87 ms, E8 6.83-6.94 vs 6.57-6.67 ms with all SMs).
+        const unsigned per = (unsigned)(ctx->sm_count * ctx->overlap2);
         const unsigned gctas = ctx->gram_ctas ? (unsigned)ctx->gram_ctas
-                                              : std::max(1u, (unsigned)(ctx->sm_count * ctx->overlap2 * 3) / 4);
+                                              : ctx->c > 16 ? std::max(1u, per * 3 / 4) : per;
         TRY(phase_gram(ctx, true, ctx->side, gctas));
         TRY(phase_allgather(ctx, buf));
         if (dual_sweep) TRY(phase_pair_pack(ctx));
