@@ -1362,6 +1362,17 @@ __global__ void __launch_bounds__(kGramMaxThreads) k_gram(Bufs b, Geo g, int dua
 
     auto issue = [&](int sidx, unsigned long long cr) {
         const int rows = (int)min((unsigned long long)R, r1 - cr);
+        if (C == C4) {
+            // unpadded rows: the chunk is one contiguous run of rows * C doubles in U and
+            // in the tile -- 16-byte copies, no per-element row / column split
+            const size_t a0 = (size_t)(g.row0 + cr) * C;
+            for (int e = 2 * threadIdx.x; e < rows * C; e += 2 * blockDim.x) {
+                cp_async16(smg + sidx * tsz + e, Bm + a0 + e);
+                if (dual) cp_async16(smg + (2 + sidx) * tsz + e, Pm + a0 + e);
+            }
+            cp_async_commit();
+            return;
+        }
         for (int e = threadIdx.x; e < rows * C4; e += blockDim.x) {
             const int rr = e / C4, cc = e % C4;
             if (cc < C) {
