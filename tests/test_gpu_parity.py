@@ -521,6 +521,25 @@ def test_stream_sweep_bitwise(oracle, monkeypatch, variant, c, weighted):
         t.close()
 
 
+@pytest.mark.parametrize("hot_mb", ["0", "0.05", "1000"])
+@pytest.mark.parametrize("c", [3, 16, 32])
+def test_hot_row_policy_bitwise(oracle, monkeypatch, hot_mb, c):
+    """FC_HOT_MB: the L2 evict_last flag (bit 31 of the stored column index) on none, some
+    or all columns -- a cache hint only: FISTA with restart and with backtracking stay
+    bitwise equal to the oracle, and so do the granular operators on the flagged CSR."""
+    monkeypatch.setenv("FC_HOT_MB", hot_mb)
+    g = ragged_graph(6000, 130 + c, True)
+    x0 = oracle.init_random(g.n, c, 5)
+    t = capi.Context(0)
+    try:
+        t.upload(g)
+        for kw in (dict(method=FISTA, max_iter=8, fista_restart=True, step_size=40 * oracle.default_step_size(g)),
+                   dict(method=FISTA_BT, max_iter=5, step_size=300 * oracle.default_step_size(g))):
+            assert_same_run(t.solve(x0, cfg(**kw)), oracle.solve(g, x0, **kw))
+    finally:
+        t.close()
+
+
 @pytest.mark.parametrize("variant", ["t2", "t2x", "tx"])
 @pytest.mark.parametrize("c", [3, 16, 20, 32])
 def test_step_t_variants_bitwise(oracle, monkeypatch, variant, c):
